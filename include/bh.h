@@ -1,0 +1,186 @@
+/*
+ * bh.h -- C ABI of libbh.so, the B200 (sm_100a) Barnes-Hut step.
+ *
+ * The library computes, per time step, the paper's data-parallel hot path
+ * (arxiv 1109.5190, PAPER.md):
+ *   - the adaptive octree, "cubes subdivided until there is one particle per
+ *     sub-cube" (§1), built from 63-bit Morton keys;
+ *   - "center of mass ... of each of the cubes";
+ *   - the force stage, "the most computationally intensive part"
+ *     (§3), with the criterion "treated as a single body only
+ *     if D is greater than r/theta" (Fig. 1);
+ *   - "compute the next iteration values" (Fig. 2c): a
+ *     kick-drift leapfrog.
+ * DESIGN.md §3 lists the readings where the paper is silent (L1-L24: r is the
+ * cell side, D is measured to the centre of mass, the test is strict, cells
+ * containing the target are always opened, Plummer softening, 21-level cap with
+ * buckets, ties sort by user index, fp64 moments in child order).
+ *
+ * Conventions for every entry point:
+ *   - Return a bh_status; BH_OK == 0.  bh_last_error(ctx) gives text.
+ *   - `where` says where caller pointers live: BH_HOST (pageable or pinned host
+ *     memory) or BH_DEVICE (device pointers on the ctx's device, e.g. a torch
+ *     tensor's data_ptr()).
+ *   - Caller arrays are only borrowed for the duration of the call.  Inputs are
+ *     copied in, outputs are written into caller buffers.
+ *   - Layouts: mass float[n]; pos, vel, acc float[n][3] row-major (x,y,z per
+ *     particle); all in USER order (the caller's particle index) unless noted.
+ *   - All device memory is carved out of the caller's `workspace`
+ *     (bh_workspace_bytes); the library never calls cudaMalloc.  The workspace
+ *     must stay allocated until bh_destroy.  Besides it the library owns only a
+ *     few hundred bytes of pinned host status memory and CUDA events.
+ *   - All device work is enqueued on params.stream (NULL: a library-owned
+ *     non-blocking stream).  bh_build_tree, bh_compute_forces with a device
+ *     output and bh_step are asynchronous; errors found on the device (non-finite
+ *     positions, infinite forces, node-capacity overflow) are reported by the
+ *     next synchronising call: bh_sync, any getter, a BH_HOST output, or the next
+ *     bh_step once the previous one has completed.
+ *   - A ctx is not thread-safe; use one ctx per device / rank.
+ */
+#ifndef BH_H
+#define BH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bh_ctx bh_ctx; /* opaque; one per rank / device */
+
+typedef enum {
+    BH_OK = 0,
+    BH_ERR_ARG = -1,       /* invalid argument; nothing was changed            */
+    BH_ERR_CUDA = -2,      /* a CUDA runtime call or kernel launch failed       */
+    BH_ERR_OOM = -3,       /* workspace too small or tree node capacity exceeded */
+    BH_ERR_STATE = -4,     /* call out of order (e.g. forces before a tree)     */
+    BH_ERR_NONFINITE = -5, /* NaN/Inf position, or eps == 0 with r == 0         */
+    BH_ERR_NCCL = -6       /* an NCCL call failed                               */
+} bh_status;
+
+enum { BH_HOST = 0, BH_DEVICE = 1 };
+
+typedef struct {
+    int64_t n;          /* particle count, 1 <= n <= 2^30 ("n particles")   */
+    double theta;       /* opening angle >= 0; 0 = never accept a cell    */
+    double eps;         /* Plummer softening >= 0 (reading L6)                               */
+    double G;           /* gravitational constant > 0 (reading L7; applied as a final scale) */
+    double dt;          /* time step > 0 (reading L8)                                       */
+    int device;         /* CUDA device ordinal                                               */
+    int rank, world;    /* Morton-range shard `rank` of `world` ranks (world == 1: one GPU) */
+    void *stream;       /* cudaStream_t for all work; NULL = library-owned stream            */
+    void *nccl_comm;    /* ncclComm_t over the `world` ranks, or NULL (see bh_step)          */
+    void *workspace;    /* device memory of >= bh_workspace_bytes(params) bytes, 256-aligned */
+    size_t workspace_bytes;
+    int64_t node_capacity; /* tree records (internal nodes + particles); 0 = default
+                              (n + max(n, min(21 n, 2^22)) + 64, which always fits
+                              n <= 199,728 and typical inputs above that)              */
+    int walk_group;     /* lanes sharing one traversal in the force walk: 0 = default (32),
+                           or 1, 2, 4, 8, 16, 32; results are identical for every value     */
+} bh_params;
+
+/* Bytes of device workspace the ctx needs for these params (n, world,
+ * node_capacity are read).  Returns 0 if the params are invalid. */
+size_t bh_workspace_bytes(const bh_params *p);
+
+/* Create a ctx and load the initial state (mass[n], pos[n][3], vel[n][3] or
+ * NULL for zero velocities), all in user order, from `where`.  Every rank
+ * passes the FULL state.  Computes the step-0 Morton order, which fixes the
+ * storage order and (world > 1) each rank's owned contiguous Morton range.
+ * Synchronises the stream. */
+bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const float *pos,
+                    const float *vel, int where);
+
+/* Replace the state (user order; vel may be NULL = zero).  Keeps the storage
+ * order of bh_create and resets the step counter (the next bh_step applies the
+ * half kick, reading L8).  Asynchronous for BH_DEVICE inputs. */
+bh_status bh_set_state(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int where);
+
+/* K0-K5: root cube, Morton keys, radix sort, octree, mass / centre of mass on
+ * the current positions.  Asynchronous. */
+bh_status bh_build_tree(bh_ctx *ctx);
+
+/* K6: accelerations a_i = G sum m_s (x_s - x_i) / (|x_s - x_i|^2 + eps^2)^(3/2)
+ * over each particle's Barnes-Hut frontier, for this rank's particles, written
+ * to acc[n][3] in user order (entries of other ranks' particles untouched).
+ * acc may be NULL (only interaction counts are produced).  Needs
+ * bh_build_tree first (BH_ERR_STATE otherwise).  Synchronises for BH_HOST. */
+bh_status bh_compute_forces(bh_ctx *ctx, float *acc, int where);
+
+/* nsteps x (K0-K5 tree, K6+K7 walk fused with the leapfrog kick-drift on this
+ * rank's particles, K8 exchange of the updated positions).  Step k == 0 of the
+ * ctx applies v += a dt/2, later steps v += a dt, then x += v dt, so after
+ * k >= 1 steps velocities are the staggered v_{k-1/2}.  With world > 1 the
+ * exchange is a grouped ncclBroadcast of every rank's slice over nccl_comm;
+ * with nccl_comm == NULL the exchange is skipped (single-GPU rank emulation:
+ * only this rank's slice advances).  Asynchronous. */
+bh_status bh_step(bh_ctx *ctx, int nsteps);
+
+/* Wait for all enqueued work; report device-side errors. */
+bh_status bh_sync(bh_ctx *ctx);
+
+/* Free the ctx (not the workspace).  NULL is a no-op. */
+bh_status bh_destroy(bh_ctx *ctx);
+
+/* ---- inspection (synchronising; user order unless noted) ---------------- */
+
+/* Positions of all particles and velocities (staggered, see bh_step) of this
+ * rank's particles; either pointer may be NULL. */
+bh_status bh_get_state(bh_ctx *ctx, float *pos, float *vel, int where);
+
+/* Root cube of the last tree: lo[3], side L and quantisation scale 2^21/L. */
+bh_status bh_get_root(bh_ctx *ctx, float *lo3, float *L, float *scale);
+
+/* Sorted 63-bit keys (Morton order) and perm[s] = user index of sorted slot s
+ * (ties by ascending user index).  Host pointers, n entries each. */
+bh_status bh_get_keys(bh_ctx *ctx, uint64_t *keys, uint32_t *perm);
+
+/* Octree in DFS pre-order (children in Morton digit order): level, first
+ * sorted particle, particle count per node, for internal nodes, level-21
+ * buckets and single-particle leaves (not bucket members).  Host pointers of
+ * `cap` entries (any may be NULL); *n_nodes receives the node count; returns
+ * BH_ERR_ARG if cap is too small (n_nodes still set). */
+bh_status bh_get_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint32_t *count,
+                      int64_t cap, int64_t *n_nodes);
+
+/* fp64 mass M and first moment MX[3] (com = MX / M) of the nodes of
+ * bh_get_tree, same order; host pointers of `cap` entries. */
+bh_status bh_get_moments(bh_ctx *ctx, double *M, double *MX, int64_t cap);
+
+/* Interactions of the last force walk (accepted cells + particles j != i,
+ * reading L21) per particle in user order (this rank's particles; NULL ok) and
+ * summed over this rank (NULL ok). */
+bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total);
+
+typedef struct {
+    int64_t n_records;      /* walk records: tree nodes + bucket members          */
+    int64_t n_internal;     /* internal nodes incl. buckets                       */
+    int64_t node_capacity;  /* capacity in records                                */
+    int64_t interactions;   /* last walk, this rank                               */
+    int64_t mac_fallbacks;  /* last walk: fp32 MAC filter inconclusive -> fp64    */
+    int64_t own_begin, own_end; /* this rank's range of storage indices          */
+    int64_t steps;          /* steps taken since create / set_state              */
+} bh_stats;
+bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);
+
+/* Per-phase device time (CUDA events on the ctx stream), accumulated over the
+ * calls made while profiling is on.  Phases: 0 bbox+keys, 1 sort, 2 tree,
+ * 3 moments, 4 walk(+integrate), 5 exchange.  ms[6], launches[6]. */
+bh_status bh_set_profiling(bh_ctx *ctx, int enable);
+bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *calls);
+
+const char *bh_last_error(const bh_ctx *ctx);
+const char *bh_status_string(int status);
+
+/* ---- NCCL bootstrap (world > 1) ----------------------------------------- */
+/* 128-byte ncclUniqueId generated on one rank and shared by the caller
+ * (e.g. a torch.distributed broadcast). */
+bh_status bh_nccl_unique_id(void *id128);
+bh_status bh_nccl_comm_init(void **comm, const void *id128, int world, int rank, int device);
+bh_status bh_nccl_comm_destroy(void *comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BH_H */

@@ -1,0 +1,326 @@
+"""Thin ctypes binding of libbh.so (include/bh.h) -- argument marshalling only.
+
+Every step of the Barnes-Hut path runs in the CUDA kernels of csrc/; this module
+only allocates the device workspace with torch (PyTorch is plumbing: device
+memory, streams, process groups), passes pointers and sizes, and raises on a
+non-zero bh_status.  There is no CPU fallback: if libbh.so is missing or no
+CUDA device is visible, every entry point raises.
+
+Names follow the ABI: bh_create / bh_set_state / bh_build_tree /
+bh_compute_forces / bh_step / bh_sync / bh_destroy and the bh_get_* getters.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libbh.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bh.h")
+
+BH_OK, BH_ERR_ARG, BH_ERR_CUDA, BH_ERR_OOM, BH_ERR_STATE, BH_ERR_NONFINITE, BH_ERR_NCCL = 0, -1, -2, -3, -4, -5, -6
+BH_HOST, BH_DEVICE = 0, 1
+PHASES = ("bbox_keys", "sort", "tree", "moments", "walk", "exchange")
+
+
+class BhParams(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("theta", C.c_double),
+        ("eps", C.c_double),
+        ("G", C.c_double),
+        ("dt", C.c_double),
+        ("device", C.c_int),
+        ("rank", C.c_int),
+        ("world", C.c_int),
+        ("stream", C.c_void_p),
+        ("nccl_comm", C.c_void_p),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_size_t),
+        ("node_capacity", C.c_int64),
+        ("walk_group", C.c_int),
+    ]
+
+
+class BhStats(C.Structure):
+    _fields_ = [
+        ("n_records", C.c_int64),
+        ("n_internal", C.c_int64),
+        ("node_capacity", C.c_int64),
+        ("interactions", C.c_int64),
+        ("mac_fallbacks", C.c_int64),
+        ("own_begin", C.c_int64),
+        ("own_end", C.c_int64),
+        ("steps", C.c_int64),
+    ]
+
+
+class BhError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_names.get(code, code)}: {msg}")
+        self.code = code
+
+
+_names = {0: "BH_OK", -1: "BH_ERR_ARG", -2: "BH_ERR_CUDA", -3: "BH_ERR_OOM", -4: "BH_ERR_STATE",
+          -5: "BH_ERR_NONFINITE", -6: "BH_ERR_NCCL"}
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libbh.so; raises if it has not been built (no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built: run `python -m paper_1109_5190_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(path)
+        vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+        P = C.POINTER(BhParams)
+        sig = {
+            "bh_workspace_bytes": (C.c_size_t, [P]),
+            "bh_create": (i32, [C.POINTER(vp), P, vp, vp, vp, i32]),
+            "bh_set_state": (i32, [vp, vp, vp, vp, i32]),
+            "bh_build_tree": (i32, [vp]),
+            "bh_compute_forces": (i32, [vp, vp, i32]),
+            "bh_step": (i32, [vp, i32]),
+            "bh_sync": (i32, [vp]),
+            "bh_destroy": (i32, [vp]),
+            "bh_get_state": (i32, [vp, vp, vp, i32]),
+            "bh_get_root": (i32, [vp, vp, vp, vp]),
+            "bh_get_keys": (i32, [vp, vp, vp]),
+            "bh_get_tree": (i32, [vp, vp, vp, vp, i64, C.POINTER(i64)]),
+            "bh_get_moments": (i32, [vp, vp, vp, i64]),
+            "bh_get_interactions": (i32, [vp, vp, vp]),
+            "bh_get_stats": (i32, [vp, C.POINTER(BhStats)]),
+            "bh_set_profiling": (i32, [vp, i32]),
+            "bh_get_profile": (i32, [vp, vp, vp, vp]),
+            "bh_last_error": (C.c_char_p, [vp]),
+            "bh_status_string": (C.c_char_p, [i32]),
+            "bh_nccl_unique_id": (i32, [vp]),
+            "bh_nccl_comm_init": (i32, [C.POINTER(vp), vp, i32, i32, i32]),
+            "bh_nccl_comm_destroy": (i32, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(a.data_ptr())  # torch tensor
+
+
+def _host_f32(a, shape):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a.reshape(shape)
+
+
+class BarnesHut:
+    """One bh_ctx: a Barnes-Hut simulation state on one device (one rank)."""
+
+    def __init__(self, mass, pos, vel=None, *, theta, eps, G=1.0, dt=1e-3, device=0, rank=0, world=1,
+                 nccl_comm=None, node_capacity=0, walk_group=0, stream=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("BarnesHut needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        self.L = load_library()
+        self.torch = torch
+        on_dev = isinstance(pos, torch.Tensor) and pos.is_cuda
+        n = int(mass.shape[0])
+        self.n = n
+        self.device = device
+        torch.cuda.set_device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        p = BhParams(n=n, theta=float(theta), eps=float(eps), G=float(G), dt=float(dt), device=device, rank=rank,
+                     world=world, stream=C.c_void_p(self.stream.cuda_stream), nccl_comm=nccl_comm,
+                     workspace=None, workspace_bytes=0, node_capacity=int(node_capacity),
+                     walk_group=int(walk_group))
+        nbytes = self.L.bh_workspace_bytes(C.byref(p))
+        if nbytes == 0:
+            raise BhError(BH_ERR_ARG, "invalid parameters")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{device}")
+        base = self.workspace.data_ptr()
+        p.workspace = (base + 255) & ~255
+        p.workspace_bytes = nbytes
+        self.params = p
+        h = C.c_void_p()
+        if on_dev:
+            m_, p_, v_ = (mass.contiguous().float(), pos.contiguous().float(),
+                          None if vel is None else vel.contiguous().float())
+            rc = self.L.bh_create(C.byref(h), C.byref(p), _ptr(m_), _ptr(p_), _ptr(v_), BH_DEVICE)
+        else:
+            m_, p_ = _host_f32(mass, (n,)), _host_f32(pos, (n, 3))
+            v_ = None if vel is None else _host_f32(vel, (n, 3))
+            rc = self.L.bh_create(C.byref(h), C.byref(p), _ptr(m_), _ptr(p_), _ptr(v_), BH_HOST)
+        if rc != BH_OK:
+            raise BhError(rc, self.L.bh_last_error(None).decode())
+        self.h = h
+
+    # ------------------------------------------------------------------ utils
+    def _chk(self, rc):
+        if rc != BH_OK:
+            raise BhError(rc, self.L.bh_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.bh_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ ABI
+    def set_state(self, mass, pos, vel=None):
+        torch = self.torch
+        if isinstance(pos, torch.Tensor) and pos.is_cuda:
+            self._keep = (mass.contiguous().float(), pos.contiguous().float(),
+                          None if vel is None else vel.contiguous().float())
+            self._chk(self.L.bh_set_state(self.h, *map(_ptr, self._keep), BH_DEVICE))
+        else:
+            n = self.n
+            m_, p_ = _host_f32(mass, (n,)), _host_f32(pos, (n, 3))
+            v_ = None if vel is None else _host_f32(vel, (n, 3))
+            self._chk(self.L.bh_set_state(self.h, _ptr(m_), _ptr(p_), _ptr(v_), BH_HOST))
+            self._chk(self.L.bh_sync(self.h))
+
+    def build_tree(self):
+        self._chk(self.L.bh_build_tree(self.h))
+
+    def compute_forces(self, out=None):
+        """Accelerations [n,3] (user order).  `out`: a CUDA tensor to fill
+        asynchronously; default returns a host numpy array."""
+        if out is not None:
+            self._chk(self.L.bh_compute_forces(self.h, _ptr(out), BH_DEVICE))
+            return out
+        a = np.zeros((self.n, 3), np.float32)
+        self._chk(self.L.bh_compute_forces(self.h, _ptr(a), BH_HOST))
+        return a
+
+    def step(self, nsteps=1):
+        self._chk(self.L.bh_step(self.h, int(nsteps)))
+
+    def sync(self):
+        self._chk(self.L.bh_sync(self.h))
+
+    def get_state(self, pos_out=None, vel_out=None):
+        if pos_out is not None or vel_out is not None:
+            self._chk(self.L.bh_get_state(self.h, _ptr(pos_out), _ptr(vel_out), BH_DEVICE))
+            return pos_out, vel_out
+        pos = np.zeros((self.n, 3), np.float32)
+        vel = np.zeros((self.n, 3), np.float32)
+        self._chk(self.L.bh_get_state(self.h, _ptr(pos), _ptr(vel), BH_HOST))
+        return pos, vel
+
+    def get_root(self):
+        lo = np.zeros(3, np.float32)
+        Lv = np.zeros(1, np.float32)
+        sc = np.zeros(1, np.float32)
+        self._chk(self.L.bh_get_root(self.h, _ptr(lo), _ptr(Lv), _ptr(sc)))
+        return lo, Lv[0], sc[0]
+
+    def get_keys(self):
+        k = np.zeros(self.n, np.uint64)
+        perm = np.zeros(self.n, np.uint32)
+        self._chk(self.L.bh_get_keys(self.h, _ptr(k), _ptr(perm)))
+        return k, perm
+
+    def get_tree(self):
+        nn = C.c_int64(0)
+        rc = self.L.bh_get_tree(self.h, None, None, None, 0, C.byref(nn))
+        if rc not in (BH_OK, BH_ERR_ARG):
+            self._chk(rc)
+        m = nn.value
+        lv = np.zeros(m, np.uint8)
+        fi = np.zeros(m, np.uint32)
+        co = np.zeros(m, np.uint32)
+        self._chk(self.L.bh_get_tree(self.h, _ptr(lv), _ptr(fi), _ptr(co), m, C.byref(nn)))
+        return lv, fi, co
+
+    def get_moments(self):
+        nn = C.c_int64(0)
+        rc = self.L.bh_get_tree(self.h, None, None, None, 0, C.byref(nn))
+        if rc not in (BH_OK, BH_ERR_ARG):
+            self._chk(rc)
+        m = nn.value
+        M = np.zeros(m, np.float64)
+        MX = np.zeros((m, 3), np.float64)
+        self._chk(self.L.bh_get_moments(self.h, _ptr(M), _ptr(MX), m))
+        return M, MX
+
+    def get_interactions(self):
+        c = np.zeros(self.n, np.uint32)
+        tot = C.c_uint64(0)
+        self._chk(self.L.bh_get_interactions(self.h, _ptr(c), C.c_void_p(C.addressof(tot))))
+        return c, int(tot.value)
+
+    def get_stats(self) -> dict:
+        s = BhStats()
+        self._chk(self.L.bh_get_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in BhStats._fields_}
+
+    def set_profiling(self, on=True):
+        self._chk(self.L.bh_set_profiling(self.h, 1 if on else 0))
+
+    def get_profile(self) -> dict:
+        ms = np.zeros(6, np.float64)
+        ln = np.zeros(6, np.int64)
+        calls = np.zeros(1, np.int64)
+        self._chk(self.L.bh_get_profile(self.h, _ptr(ms), _ptr(ln), _ptr(calls)))
+        return {"ms": dict(zip(PHASES, ms.tolist())), "launches": dict(zip(PHASES, ln.tolist())),
+                "calls": int(calls[0])}
+
+
+# module-level aliases with the ABI names
+def bh_create(mass, pos, vel=None, **kw) -> BarnesHut:
+    return BarnesHut(mass, pos, vel, **kw)
+
+
+def bh_build_tree(ctx: BarnesHut):
+    ctx.build_tree()
+
+
+def bh_compute_forces(ctx: BarnesHut, out=None):
+    return ctx.compute_forces(out)
+
+
+def bh_step(ctx: BarnesHut, nsteps=1):
+    ctx.step(nsteps)
+
+
+def bh_destroy(ctx: BarnesHut):
+    ctx.close()
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = (C.c_ubyte * 128)()
+    rc = L.bh_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc != BH_OK:
+        raise BhError(rc, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def nccl_comm_init(uid: bytes, world: int, rank: int, device: int):
+    L = load_library()
+    buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+    comm = C.c_void_p()
+    rc = L.bh_nccl_comm_init(C.byref(comm), C.cast(buf, C.c_void_p), world, rank, device)
+    if rc != BH_OK:
+        raise BhError(rc, "ncclCommInitRank failed")
+    return comm
+
+
+def nccl_comm_destroy(comm):
+    load_library().bh_nccl_comm_destroy(comm)

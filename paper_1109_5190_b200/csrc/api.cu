@@ -1,0 +1,853 @@
+// api.cu -- the C ABI of libbh.so (include/bh.h): ctx, workspace carving,
+// state load / store, the step driver and the NCCL exchange (K8).
+//
+// The step driver enqueues, per time step ("a global barrier
+// at the tree construction stage of every iteration" = stream order here):
+//   K0 bbox -> K1 keys (+ sort histograms) -> K2 8 Onesweep passes (+ tie
+//   fix-up) -> K4 LCP / record counts / scan / emit -> K5 22 level passes ->
+//   [world > 1: owned-target compaction] -> K6+K7 walk + leapfrog ->
+//   [world > 1: K8 grouped ncclBroadcast of every rank's slice of pos4].
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "bh_internal.cuh"
+
+using namespace bh;
+
+struct ProfPair {
+  cudaEvent_t a, b;
+  int phase;
+  int launches;
+};
+
+struct bh_ctx {
+  bh_params p;
+  Layout lay;
+  Workspace W;
+  cudaStream_t stream;
+  bool own_stream;
+  int64_t own_lo, own_hi;
+  int64_t steps;
+  bool tree_valid;
+  bool walked;
+  int sort_buf;
+  DevStatus *hstatus;  // pinned
+  cudaEvent_t status_ev;
+  bool status_pending;
+  char err[512];
+  // profiling
+  bool prof;
+  std::vector<ProfPair> pending;
+  std::vector<cudaEvent_t> free_events;
+  double prof_ms[BH_NPHASE];
+  int64_t prof_launches[BH_NPHASE];
+  int64_t prof_calls;
+};
+
+static bh_status fail(bh_ctx *c, bh_status st, const char *fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof c->err, fmt, ap);
+    va_end(ap);
+  }
+  return st;
+}
+
+#define CK(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(ctx, BH_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                      \
+  } while (0)
+
+// ---------------------------------------------------------------- layout
+namespace bh {
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout make_layout(int64_t n, int world, int64_t node_capacity) {
+  Layout L;
+  memset(&L, 0, sizeof L);
+  L.n = n;
+  int64_t def_int = n;
+  int64_t worst = 21 * n;
+  if (worst > ((int64_t)1 << 22)) worst = (int64_t)1 << 22;
+  if (worst > def_int) def_int = worst;
+  L.cap_rec = node_capacity > 0 ? node_capacity : n + def_int + 64;
+  L.cap_int = L.cap_rec - n;
+  L.n_own_max = (n + world - 1) / world + 1;
+  L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
+  L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+  size_t sz[21] = {
+      sizeof(DevStatus),                       // 0 status
+      (size_t)n * 16,                          // 1 pos4
+      (size_t)L.n_own_max * 16,                // 2 vel4
+      (size_t)n * 4,                           // 3 uid
+      (size_t)n * 8,                           // 4 keys0
+      (size_t)n * 8,                           // 5 keys1
+      (size_t)n * 4,                           // 6 vals0
+      (size_t)n * 4,                           // 7 vals1
+      (size_t)n,                               // 8 lcp
+      (size_t)(n + 1) * 4,                     // 9 nstart
+      (size_t)n * 4,                           // 10 icount
+      (size_t)n * 12,                          // 11 accu
+      (size_t)(n + 1) * 4,                     // 12 targets
+      (size_t)L.scan_tiles * 4,                // 13 scan_tmp
+      sizeof(uint32_t) * (SORT_PASSES * SORT_RADIX + 8 + (size_t)SORT_PASSES * L.sort_tiles * SORT_RADIX),  // 14
+      sizeof(float) * 8 * BBOX_BLOCKS,         // 15 bbox partials
+      (size_t)L.cap_rec * 16,                  // 16 rec_cm
+      (size_t)L.cap_rec * 16,                  // 17 rec_aux
+      (size_t)L.cap_rec * 4,                   // 18 rec_first
+      (size_t)L.cap_rec * 32,                  // 19 rec_mom
+      (size_t)L.cap_int * 4,                   // 20 lvl_list
+  };
+  size_t off = 0;
+  for (int i = 0; i < 21; i++) {
+    L.off[i] = off;
+    off += align_up(sz[i]);
+  }
+  L.total = off;
+  return L;
+}
+
+void bind_workspace(const Layout &L, void *base, Workspace &W) {
+  char *b = (char *)base;
+  W.status = (DevStatus *)(b + L.off[0]);
+  W.pos4 = (float4 *)(b + L.off[1]);
+  W.vel4 = (float4 *)(b + L.off[2]);
+  W.uid = (uint32_t *)(b + L.off[3]);
+  W.keys[0] = (unsigned long long *)(b + L.off[4]);
+  W.keys[1] = (unsigned long long *)(b + L.off[5]);
+  W.vals[0] = (uint32_t *)(b + L.off[6]);
+  W.vals[1] = (uint32_t *)(b + L.off[7]);
+  W.lcp = (uint8_t *)(b + L.off[8]);
+  W.nstart = (uint32_t *)(b + L.off[9]);
+  W.icount = (uint32_t *)(b + L.off[10]);
+  W.accu = (float *)(b + L.off[11]);
+  W.targets = (uint32_t *)(b + L.off[12]);
+  W.scan_tmp = (uint32_t *)(b + L.off[13]);
+  W.sort_hist = (uint32_t *)(b + L.off[14]);
+  W.sort_tilectr = W.sort_hist + SORT_PASSES * SORT_RADIX;
+  W.sort_status = W.sort_tilectr + 8;
+  W.bbox_part = (float *)(b + L.off[15]);
+  W.rec_cm = (float4 *)(b + L.off[16]);
+  W.rec_aux = (uint4 *)(b + L.off[17]);
+  W.rec_first = (uint32_t *)(b + L.off[18]);
+  W.rec_mom = (double4 *)(b + L.off[19]);
+  W.lvl_list = (uint32_t *)(b + L.off[20]);
+}
+
+// ---------------------------------------------------------------- small kernels
+__global__ void k_pack(float4 *__restrict__ pos4, const float *__restrict__ pos, const float *__restrict__ mass,
+                       int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) pos4[i] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], mass[i]);
+}
+
+__global__ void k_iota(uint32_t *__restrict__ a, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (uint32_t)i;
+}
+
+// relabel: storage slot p takes user particle vals[p]
+__global__ void k_relabel(float4 *__restrict__ dst, const float4 *__restrict__ src_user,
+                          const uint32_t *__restrict__ vals, uint32_t *__restrict__ uid, int64_t n) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) {
+    uint32_t u = vals[p];
+    dst[p] = src_user[u];
+    uid[p] = u;
+  }
+}
+
+// storage-slot state from user-order arrays: pos4[s] = (pos[uid], mass[uid]);
+// vel4[s - lo] = vel[uid] for the own range (vel == null -> 0)
+__global__ void k_load_state(float4 *__restrict__ pos4, float4 *__restrict__ vel4, const uint32_t *__restrict__ uid,
+                             const float *__restrict__ pos, const float *__restrict__ mass,
+                             const float *__restrict__ vel, int64_t n, int64_t lo, int64_t hi) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  uint32_t u = uid[s];
+  pos4[s] = make_float4(pos[3 * (size_t)u], pos[3 * (size_t)u + 1], pos[3 * (size_t)u + 2], mass[u]);
+  if (s >= lo && s < hi)
+    vel4[s - lo] = vel ? make_float4(vel[3 * (size_t)u], vel[3 * (size_t)u + 1], vel[3 * (size_t)u + 2], 0.f)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// user-order outputs from storage slots [lo, hi): out[uid[s]] = src(s)
+__global__ void k_scatter3(float *__restrict__ out, const float4 *__restrict__ src4, const float *__restrict__ src3,
+                           const uint32_t *__restrict__ uid, int64_t lo, int64_t hi, int src_offset_lo) {
+  int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  uint32_t u = uid[s];
+  int64_t k = src_offset_lo ? s - lo : s;
+  if (src4) {
+    float4 v = src4[k];
+    out[3 * (size_t)u] = v.x; out[3 * (size_t)u + 1] = v.y; out[3 * (size_t)u + 2] = v.z;
+  } else {
+    out[3 * (size_t)u] = src3[3 * k]; out[3 * (size_t)u + 1] = src3[3 * k + 1]; out[3 * (size_t)u + 2] = src3[3 * k + 2];
+  }
+}
+
+__global__ void k_scatter1(uint32_t *__restrict__ out, const uint32_t *__restrict__ src, const uint32_t *__restrict__ uid,
+                           int64_t lo, int64_t hi) {
+  int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < hi) out[uid[s]] = src[s];
+}
+
+// owned targets: flags then compaction of the sorted positions whose storage id is own
+__global__ void k_own_flags(const uint32_t *__restrict__ vals, uint32_t *__restrict__ flag, int64_t n, uint32_t lo,
+                            uint32_t hi) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) { uint32_t s = vals[p]; flag[p] = (s >= lo && s < hi) ? 1u : 0u; }
+  if (p == n) flag[n] = 0;
+}
+__global__ void k_own_compact(const uint32_t *__restrict__ vals, const uint32_t *__restrict__ pre,
+                              uint32_t *__restrict__ targets, int64_t n, uint32_t lo, uint32_t hi) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) { uint32_t s = vals[p]; if (s >= lo && s < hi) targets[pre[p]] = (uint32_t)p; }
+}
+
+cudaError_t launch_own_targets(const Workspace &W, int64_t n, int buf, uint32_t lo, uint32_t hi, cudaStream_t s) {
+  // flags live in accu (n + 1 u32 fit in 3n floats for n >= 1)
+  uint32_t *flag = (uint32_t *)W.accu;
+  unsigned g = (unsigned)((n + 1 + 255) / 256);
+  k_own_flags<<<g, 256, 0, s>>>(W.vals[buf], flag, n, lo, hi);
+  cudaError_t e = launch_scan_u32(flag, n + 1, W.scan_tmp, s);
+  if (e != cudaSuccess) return e;
+  k_own_compact<<<g, 256, 0, s>>>(W.vals[buf], flag, W.targets, n, lo, hi);
+  return cudaGetLastError();
+}
+
+}  // namespace bh
+
+// ---------------------------------------------------------------- helpers
+static unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1); }
+
+static bh_status validate(const bh_params *p, char *err, size_t errn) {
+  if (!p) { snprintf(err, errn, "null params"); return BH_ERR_ARG; }
+  if (p->n < 1 || p->n > ((int64_t)1 << 30)) { snprintf(err, errn, "n must be in [1, 2^30]"); return BH_ERR_ARG; }
+  if (!(p->theta >= 0.0) || !(p->eps >= 0.0) || !(p->G > 0.0) || !(p->dt > 0.0)) {
+    snprintf(err, errn, "need theta >= 0, eps >= 0, G > 0, dt > 0");
+    return BH_ERR_ARG;
+  }
+  if (p->world < 1 || p->rank < 0 || p->rank >= p->world || p->world > p->n) {
+    snprintf(err, errn, "need 0 <= rank < world <= n");
+    return BH_ERR_ARG;
+  }
+  if (p->node_capacity != 0 && p->node_capacity < p->n + 1) {
+    snprintf(err, errn, "node_capacity must be 0 or >= n + 1");
+    return BH_ERR_ARG;
+  }
+  int g = p->walk_group;
+  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32)) {
+    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16 or 32");
+    return BH_ERR_ARG;
+  }
+  return BH_OK;
+}
+
+static thread_local char g_err[512];
+
+static cudaEvent_t take_event(bh_ctx *ctx) {
+  if (!ctx->free_events.empty()) {
+    cudaEvent_t e = ctx->free_events.back();
+    ctx->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+static void prof_begin(bh_ctx *ctx, ProfPair *pp, int phase) {
+  if (!ctx->prof) return;
+  pp->a = take_event(ctx);
+  pp->b = take_event(ctx);
+  pp->phase = phase;
+  pp->launches = 0;
+  cudaEventRecord(pp->a, ctx->stream);
+}
+static void prof_end(bh_ctx *ctx, ProfPair *pp, int launches) {
+  if (!ctx->prof) return;
+  cudaEventRecord(pp->b, ctx->stream);
+  pp->launches = launches;
+  ctx->pending.push_back(*pp);
+}
+static void prof_collect(bh_ctx *ctx) {
+  for (auto &pp : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pp.a, pp.b) == cudaSuccess) ctx->prof_ms[pp.phase] += ms;
+    ctx->prof_launches[pp.phase] += pp.launches;
+    ctx->free_events.push_back(pp.a);
+    ctx->free_events.push_back(pp.b);
+  }
+  ctx->pending.clear();
+}
+
+static bh_status status_from_device(bh_ctx *ctx) {
+  uint32_t e = ctx->hstatus->err;
+  if (e & ERR_NONFINITE_POS) return fail(ctx, BH_ERR_NONFINITE, "non-finite position or mass in the state");
+  if (e & ERR_NODE_OVERFLOW)
+    return fail(ctx, BH_ERR_OOM, "tree needs %u records (> node_capacity %lld); raise bh_params.node_capacity",
+                ctx->hstatus->n_records, (long long)ctx->lay.cap_rec);
+  if (e & ERR_NONFINITE_FORCE)
+    return fail(ctx, BH_ERR_NONFINITE, "eps == 0 and two particles coincide: infinite force");
+  return BH_OK;
+}
+
+static bh_status enqueue_status(bh_ctx *ctx) {
+  CK(cudaMemcpyAsync(ctx->hstatus, ctx->W.status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaEventRecord(ctx->status_ev, ctx->stream));
+  ctx->status_pending = true;
+  return BH_OK;
+}
+
+static bh_status do_sync(bh_ctx *ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->status_pending) ctx->status_pending = false;
+  CK(cudaMemcpy(ctx->hstatus, ctx->W.status, sizeof(DevStatus), cudaMemcpyDeviceToHost));
+  if (ctx->prof) prof_collect(ctx);
+  return status_from_device(ctx);
+}
+
+static bh_status set_dev(bh_ctx *ctx) {
+  CK(cudaSetDevice(ctx->p.device));
+  return BH_OK;
+}
+
+// K0-K5 on the current pos4
+static bh_status build_tree(bh_ctx *ctx) {
+  const int64_t n = ctx->p.n;
+  cudaStream_t s = ctx->stream;
+  ProfPair pp;
+  // clear per-build counters (interactions/fallbacks are per walk)
+  prof_begin(ctx, &pp, 0);
+  CK(launch_bbox(ctx->W, n, s));
+  CK(launch_keys(ctx->W, n, s));
+  prof_end(ctx, &pp, 3);
+  prof_begin(ctx, &pp, 1);
+  int buf = 0;
+  CK(launch_sort(ctx->W, n, s, &buf));
+  CK(launch_tie_fixup(ctx->W, n, buf, s));
+  prof_end(ctx, &pp, SORT_PASSES + 1);
+  ctx->sort_buf = buf;
+  prof_begin(ctx, &pp, 2);
+  CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, s));
+  prof_end(ctx, &pp, 6);
+  prof_begin(ctx, &pp, 3);
+  int launches = 0;
+  CK(launch_moments(ctx->W, n, ctx->lay.cap_rec, ctx->lay.cap_int, ctx->p.theta, s, &launches));
+  prof_end(ctx, &pp, launches);
+  ctx->tree_valid = true;
+  return BH_OK;
+}
+
+static bh_status walk(bh_ctx *ctx, int mode, float kick) {
+  const int64_t n = ctx->p.n;
+  cudaStream_t s = ctx->stream;
+  ProfPair pp;
+  prof_begin(ctx, &pp, 4);
+  int launches = 1;
+  WalkArgs a;
+  memset(&a, 0, sizeof a);
+  a.n = n;
+  a.buf = ctx->sort_buf;
+  a.group = ctx->p.walk_group ? ctx->p.walk_group : 32;
+  a.mode = mode;
+  a.eps2 = (float)(ctx->p.eps * ctx->p.eps);
+  a.G = (float)ctx->p.G;
+  a.kick = kick;
+  a.dt = (float)ctx->p.dt;
+  a.theta2 = ctx->p.theta * ctx->p.theta;
+  a.own_lo = (uint32_t)ctx->own_lo;
+  a.acc_out = mode == 0 ? ctx->W.accu : nullptr;
+  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 2 * sizeof(unsigned long long), s));
+  if (ctx->p.world > 1) {
+    CK(launch_own_targets(ctx->W, n, ctx->sort_buf, (uint32_t)ctx->own_lo, (uint32_t)ctx->own_hi, s));
+    a.use_targets = 1;
+    a.n_targets = ctx->own_hi - ctx->own_lo;
+    launches += 4;
+  } else {
+    a.use_targets = 0;
+    a.n_targets = n;
+  }
+  CK(launch_walk(ctx->W, a, s));
+  prof_end(ctx, &pp, launches);
+  ctx->walked = true;
+  return BH_OK;
+}
+
+static bh_status exchange(bh_ctx *ctx) {
+  if (ctx->p.world == 1 || !ctx->p.nccl_comm) return BH_OK;
+  ProfPair pp;
+  prof_begin(ctx, &pp, 5);
+  ncclComm_t comm = (ncclComm_t)ctx->p.nccl_comm;
+  const int64_t n = ctx->p.n;
+  const int P = ctx->p.world;
+  if (ncclGroupStart() != ncclSuccess) return fail(ctx, BH_ERR_NCCL, "ncclGroupStart failed");
+  for (int r = 0; r < P; r++) {
+    int64_t lo = n * r / P, hi = n * (r + 1) / P;
+    if (hi <= lo) continue;
+    float *buf = (float *)(ctx->W.pos4 + lo);
+    ncclResult_t rc = ncclBroadcast(buf, buf, (size_t)(hi - lo) * 4, ncclFloat, r, comm, ctx->stream);
+    if (rc != ncclSuccess) {
+      ncclGroupEnd();
+      return fail(ctx, BH_ERR_NCCL, "ncclBroadcast: %s", ncclGetErrorString(rc));
+    }
+  }
+  ncclResult_t rc = ncclGroupEnd();
+  if (rc != ncclSuccess) return fail(ctx, BH_ERR_NCCL, "ncclGroupEnd: %s", ncclGetErrorString(rc));
+  prof_end(ctx, &pp, 1);
+  return BH_OK;
+}
+
+// copy caller inputs (user order) into device scratch: pos -> accu, mass -> targets,
+// vel -> rec_aux region; returns device pointers
+static bh_status stage_inputs(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int where,
+                              const float **dm, const float **dp, const float **dv) {
+  const int64_t n = ctx->p.n;
+  if (where == BH_DEVICE) {
+    *dm = mass; *dp = pos; *dv = vel;
+    return BH_OK;
+  }
+  float *sp = ctx->W.accu;
+  float *sm = (float *)ctx->W.targets;
+  float *sv = (float *)ctx->W.rec_aux;
+  CK(cudaMemcpyAsync(sp, pos, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(sm, mass, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (vel) CK(cudaMemcpyAsync(sv, vel, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
+  *dm = sm; *dp = sp; *dv = vel ? sv : nullptr;
+  return BH_OK;
+}
+
+// ---------------------------------------------------------------- ABI
+extern "C" {
+
+size_t bh_workspace_bytes(const bh_params *p) {
+  char e[128];
+  if (validate(p, e, sizeof e) != BH_OK) return 0;
+  return make_layout(p->n, p->world, p->node_capacity).total;
+}
+
+const char *bh_status_string(int st) {
+  switch (st) {
+    case BH_OK: return "BH_OK";
+    case BH_ERR_ARG: return "BH_ERR_ARG";
+    case BH_ERR_CUDA: return "BH_ERR_CUDA";
+    case BH_ERR_OOM: return "BH_ERR_OOM";
+    case BH_ERR_STATE: return "BH_ERR_STATE";
+    case BH_ERR_NONFINITE: return "BH_ERR_NONFINITE";
+    case BH_ERR_NCCL: return "BH_ERR_NCCL";
+    default: return "BH_UNKNOWN";
+  }
+}
+
+const char *bh_last_error(const bh_ctx *ctx) { return ctx ? ctx->err : g_err; }
+
+bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const float *pos, const float *vel,
+                    int where) {
+  if (!out) { snprintf(g_err, sizeof g_err, "null out"); return BH_ERR_ARG; }
+  *out = nullptr;
+  bh_status v = validate(p, g_err, sizeof g_err);
+  if (v != BH_OK) return v;
+  if (!mass || !pos || (where != BH_HOST && where != BH_DEVICE)) {
+    snprintf(g_err, sizeof g_err, "need mass, pos and where in {BH_HOST, BH_DEVICE}");
+    return BH_ERR_ARG;
+  }
+  Layout lay = make_layout(p->n, p->world, p->node_capacity);
+  if (!p->workspace || p->workspace_bytes < lay.total || ((uintptr_t)p->workspace & 255)) {
+    snprintf(g_err, sizeof g_err, "workspace must be 256-aligned and >= %zu bytes", lay.total);
+    return BH_ERR_OOM;
+  }
+  bh_ctx *ctx = new bh_ctx();
+  ctx->p = *p;
+  ctx->lay = lay;
+  ctx->err[0] = 0;
+  ctx->prof = false;
+  ctx->prof_calls = 0;
+  memset(ctx->prof_ms, 0, sizeof ctx->prof_ms);
+  memset(ctx->prof_launches, 0, sizeof ctx->prof_launches);
+  bind_workspace(lay, p->workspace, ctx->W);
+  const int64_t n = p->n;
+  ctx->own_lo = n * p->rank / p->world;
+  ctx->own_hi = n * (p->rank + 1) / p->world;
+  ctx->steps = 0;
+  ctx->tree_valid = false;
+  ctx->walked = false;
+  ctx->sort_buf = 0;
+  ctx->status_pending = false;
+  bh_status st = BH_OK;
+  do {
+    if (cudaSetDevice(p->device) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "cudaSetDevice(%d) failed", p->device); break; }
+    if (p->stream) {
+      ctx->stream = (cudaStream_t)p->stream;
+      ctx->own_stream = false;
+    } else {
+      if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "stream create failed"); break; }
+      ctx->own_stream = true;
+    }
+    if (cudaMallocHost(&ctx->hstatus, sizeof(DevStatus)) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "pinned alloc failed"); break; }
+    if (cudaEventCreateWithFlags(&ctx->status_ev, cudaEventDisableTiming) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "event create failed"); break; }
+    cudaStream_t s = ctx->stream;
+    if (cudaMemsetAsync(ctx->W.status, 0, sizeof(DevStatus), s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
+    const float *dm, *dp, *dv;
+    st = stage_inputs(ctx, mass, pos, vel, where, &dm, &dp, &dv);
+    if (st) break;
+    // user-order pos4 -> step-0 Morton order -> storage order
+    k_pack<<<blocks_for(n), 256, 0, s>>>(ctx->W.pos4, dp, dm, n);
+    k_iota<<<blocks_for(n), 256, 0, s>>>(ctx->W.uid, n);
+    if (cudaGetLastError() != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "pack launch failed"); break; }
+    // velocities (user order) parked as float4 in rec_mom (>= 32 B per particle)
+    float4 *vtmp = (float4 *)ctx->W.rec_mom;
+    if (dv) {
+      k_pack<<<blocks_for(n), 256, 0, s>>>(vtmp, dv, dm, n);  // .w = mass, ignored
+    }
+    if (launch_bbox(ctx->W, n, s) != cudaSuccess || launch_keys(ctx->W, n, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "keys launch failed"); break; }
+    int buf = 0;
+    if (launch_sort(ctx->W, n, s, &buf) != cudaSuccess || launch_tie_fixup(ctx->W, n, buf, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "sort launch failed"); break; }
+    // relabel: gather user-order pos4 into rec_cm, copy back; uid[p] = user index
+    k_relabel<<<blocks_for(n), 256, 0, s>>>(ctx->W.rec_cm, ctx->W.pos4, ctx->W.vals[buf], ctx->W.uid, n);
+    if (cudaMemcpyAsync(ctx->W.pos4, ctx->W.rec_cm, (size_t)n * 16, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "copy failed"); break; }
+    int64_t own_n = ctx->own_hi - ctx->own_lo;
+    if (dv) {
+      // vel4[s - lo] = vtmp[uid[s]] for own s: reuse relabel into rec_cm then copy the own slice
+      k_relabel<<<blocks_for(n), 256, 0, s>>>(ctx->W.rec_cm, vtmp, ctx->W.vals[buf], ctx->W.uid, n);
+      if (cudaMemcpyAsync(ctx->W.vel4, ctx->W.rec_cm + ctx->own_lo, (size_t)own_n * 16, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "copy failed"); break; }
+    } else {
+      if (cudaMemsetAsync(ctx->W.vel4, 0, (size_t)own_n * 16, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
+    }
+    if (cudaMemsetAsync(ctx->W.icount, 0, (size_t)n * 4, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
+    st = do_sync(ctx);
+  } while (0);
+  if (st != BH_OK) {
+    snprintf(g_err, sizeof g_err, "%s", ctx->err);
+    bh_destroy(ctx);
+    return st;
+  }
+  *out = ctx;
+  return BH_OK;
+}
+
+bh_status bh_set_state(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int where) {
+  if (!ctx || !mass || !pos || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  const int64_t n = ctx->p.n;
+  const float *dm, *dp, *dv;
+  st = stage_inputs(ctx, mass, pos, vel, where, &dm, &dp, &dv);
+  if (st) return st;
+  k_load_state<<<blocks_for(n), 256, 0, ctx->stream>>>(ctx->W.pos4, ctx->W.vel4, ctx->W.uid, dp, dm, dv, n,
+                                                        ctx->own_lo, ctx->own_hi);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(&ctx->W.status->err, 0, sizeof(uint32_t), ctx->stream));
+  ctx->steps = 0;
+  ctx->tree_valid = false;
+  return BH_OK;
+}
+
+bh_status bh_build_tree(bh_ctx *ctx) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  if (ctx->prof) ctx->prof_calls++;
+  st = build_tree(ctx);
+  if (st) return st;
+  return enqueue_status(ctx);
+}
+
+bh_status bh_compute_forces(bh_ctx *ctx, float *acc, int where) {
+  if (!ctx || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  if (!ctx->tree_valid) return fail(ctx, BH_ERR_STATE, "bh_compute_forces needs bh_build_tree on the current state");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = walk(ctx, 0, 0.f);
+  if (st) return st;
+  const int64_t lo = ctx->own_lo, hi = ctx->own_hi, own_n = hi - lo;
+  if (acc && where == BH_DEVICE) {
+    k_scatter3<<<blocks_for(own_n), 256, 0, ctx->stream>>>(acc, nullptr, ctx->W.accu, ctx->W.uid, lo, hi, 1);
+    CK(cudaGetLastError());
+    return enqueue_status(ctx);
+  }
+  if (acc) {
+    // storage-order own slice + uid slice to host, scatter on the host
+    std::vector<float> a((size_t)own_n * 3);
+    std::vector<uint32_t> u((size_t)own_n);
+    CK(cudaMemcpyAsync(a.data(), ctx->W.accu, (size_t)own_n * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(u.data(), ctx->W.uid + lo, (size_t)own_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    st = do_sync(ctx);
+    if (st) return st;
+    for (int64_t k = 0; k < own_n; k++) {
+      size_t ui = u[k];
+      acc[3 * ui] = a[3 * k]; acc[3 * ui + 1] = a[3 * k + 1]; acc[3 * ui + 2] = a[3 * k + 2];
+    }
+    return BH_OK;
+  }
+  return enqueue_status(ctx);
+}
+
+bh_status bh_step(bh_ctx *ctx, int nsteps) {
+  if (!ctx || nsteps < 0) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  if (ctx->status_pending && cudaEventQuery(ctx->status_ev) == cudaSuccess) {
+    ctx->status_pending = false;
+    st = status_from_device(ctx);
+    if (st) return st;
+  }
+  for (int k = 0; k < nsteps; k++) {
+    if (ctx->prof) ctx->prof_calls++;
+    st = build_tree(ctx);
+    if (st) return st;
+    float kick = (float)(ctx->steps == 0 ? 0.5 * ctx->p.dt : ctx->p.dt);
+    st = walk(ctx, 1, kick);
+    if (st) return st;
+    st = exchange(ctx);
+    if (st) return st;
+    ctx->steps++;
+    ctx->tree_valid = false;
+  }
+  return enqueue_status(ctx);
+}
+
+bh_status bh_sync(bh_ctx *ctx) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  return do_sync(ctx);
+}
+
+bh_status bh_destroy(bh_ctx *ctx) {
+  if (!ctx) return BH_OK;
+  cudaSetDevice(ctx->p.device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto &pp : ctx->pending) { cudaEventDestroy(pp.a); cudaEventDestroy(pp.b); }
+  for (auto e : ctx->free_events) cudaEventDestroy(e);
+  if (ctx->status_ev) cudaEventDestroy(ctx->status_ev);
+  if (ctx->hstatus) cudaFreeHost(ctx->hstatus);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return BH_OK;
+}
+
+bh_status bh_get_state(bh_ctx *ctx, float *pos, float *vel, int where) {
+  if (!ctx || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  const int64_t n = ctx->p.n, lo = ctx->own_lo, hi = ctx->own_hi, own_n = hi - lo;
+  cudaStream_t s = ctx->stream;
+  if (pos) {
+    float *dst = where == BH_DEVICE ? pos : ctx->W.accu;
+    k_scatter3<<<blocks_for(n), 256, 0, s>>>(dst, ctx->W.pos4, nullptr, ctx->W.uid, 0, n, 0);
+    CK(cudaGetLastError());
+    if (where == BH_HOST) CK(cudaMemcpyAsync(pos, ctx->W.accu, (size_t)n * 12, cudaMemcpyDeviceToHost, s));
+  }
+  if (vel) {
+    if (where == BH_DEVICE) {
+      k_scatter3<<<blocks_for(own_n), 256, 0, s>>>(vel, ctx->W.vel4, nullptr, ctx->W.uid, lo, hi, 1);
+      CK(cudaGetLastError());
+    } else {
+      std::vector<float4> v((size_t)own_n);
+      std::vector<uint32_t> u((size_t)own_n);
+      CK(cudaMemcpyAsync(v.data(), ctx->W.vel4, (size_t)own_n * 16, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(u.data(), ctx->W.uid + lo, (size_t)own_n * 4, cudaMemcpyDeviceToHost, s));
+      st = do_sync(ctx);
+      if (st) return st;
+      for (int64_t k = 0; k < own_n; k++) {
+        size_t ui = u[k];
+        vel[3 * ui] = v[k].x; vel[3 * ui + 1] = v[k].y; vel[3 * ui + 2] = v[k].z;
+      }
+    }
+  }
+  return do_sync(ctx);
+}
+
+bh_status bh_get_root(bh_ctx *ctx, float *lo3, float *L, float *scale) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  if (st) return st;
+  for (int a = 0; a < 3; a++) if (lo3) lo3[a] = ctx->hstatus->lo[a];
+  if (L) *L = ctx->hstatus->L;
+  if (scale) *scale = ctx->hstatus->scale;
+  return BH_OK;
+}
+
+bh_status bh_get_keys(bh_ctx *ctx, uint64_t *keys, uint32_t *perm) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  const int64_t n = ctx->p.n;
+  cudaStream_t s = ctx->stream;
+  if (keys) CK(cudaMemcpyAsync(keys, ctx->W.keys[ctx->sort_buf], (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  if (perm) {
+    std::vector<uint32_t> v((size_t)n), u((size_t)n);
+    CK(cudaMemcpyAsync(v.data(), ctx->W.vals[ctx->sort_buf], (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(u.data(), ctx->W.uid, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    st = do_sync(ctx);
+    if (st) return st;
+    for (int64_t p = 0; p < n; p++) perm[p] = u[v[p]];
+    return BH_OK;
+  }
+  return do_sync(ctx);
+}
+
+static bh_status export_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint32_t *count, double *M, double *MX,
+                             int64_t cap, int64_t *n_nodes) {
+  // copy the raw records back and re-format on the host (inspection only):
+  // drop bucket-member records, count = first(skip) - first, leaf moments (m, m x)
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  if (st) return st;
+  const int64_t n = ctx->p.n;
+  const uint32_t nrec = ctx->hstatus->n_records;
+  std::vector<uint4> aux(nrec);
+  std::vector<uint32_t> fst(nrec);
+  std::vector<float4> cm;
+  std::vector<double4> mom;
+  CK(cudaMemcpy(aux.data(), ctx->W.rec_aux, (size_t)nrec * 16, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(fst.data(), ctx->W.rec_first, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
+  if (M || MX) {
+    cm.resize(nrec);
+    mom.resize(nrec);
+    CK(cudaMemcpy(cm.data(), ctx->W.rec_cm, (size_t)nrec * 16, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(mom.data(), ctx->W.rec_mom, (size_t)nrec * 32, cudaMemcpyDeviceToHost));
+  }
+  int64_t k = 0;
+  for (uint32_t c = 0; c < nrec; c++) {
+    const uint4 a = aux[c];
+    if (a.w & META_MEMBER) continue;
+    if (k < cap) {
+      const bool leaf = (a.w & META_LEAF) != 0;
+      if (level) level[k] = (uint8_t)(a.w & META_LEVEL_MASK);
+      if (first) first[k] = fst[c];
+      if (count) count[k] = leaf ? 1u : (uint32_t)((a.z >= nrec ? (uint32_t)n : fst[a.z]) - fst[c]);
+      if (M || MX) {
+        double m, x, y, z;
+        if (leaf) {
+          m = (double)cm[c].w;
+          x = m * (double)cm[c].x; y = m * (double)cm[c].y; z = m * (double)cm[c].z;
+        } else {
+          m = mom[c].x; x = mom[c].y; y = mom[c].z; z = mom[c].w;
+        }
+        if (M) M[k] = m;
+        if (MX) { MX[3 * k] = x; MX[3 * k + 1] = y; MX[3 * k + 2] = z; }
+      }
+    }
+    k++;
+  }
+  if (n_nodes) *n_nodes = k;
+  if (k > cap) return fail(ctx, BH_ERR_ARG, "cap %lld < %lld tree nodes", (long long)cap, (long long)k);
+  return BH_OK;
+}
+
+bh_status bh_get_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint32_t *count, int64_t cap, int64_t *n_nodes) {
+  if (!ctx) return BH_ERR_ARG;
+  if (!ctx->tree_valid && ctx->steps == 0) return fail(ctx, BH_ERR_STATE, "no tree built yet");
+  return export_tree(ctx, level, first, count, nullptr, nullptr, cap, n_nodes);
+}
+
+bh_status bh_get_moments(bh_ctx *ctx, double *M, double *MX, int64_t cap) {
+  if (!ctx) return BH_ERR_ARG;
+  if (!ctx->tree_valid && ctx->steps == 0) return fail(ctx, BH_ERR_STATE, "no tree built yet");
+  int64_t nn = 0;
+  return export_tree(ctx, nullptr, nullptr, nullptr, M, MX, cap, &nn);
+}
+
+bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  const int64_t lo = ctx->own_lo, hi = ctx->own_hi, own_n = hi - lo;
+  if (count) {
+    std::vector<uint32_t> c((size_t)own_n), u((size_t)own_n);
+    CK(cudaMemcpyAsync(c.data(), ctx->W.icount + lo, (size_t)own_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(u.data(), ctx->W.uid + lo, (size_t)own_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    st = do_sync(ctx);
+    if (st) return st;
+    for (int64_t k = 0; k < own_n; k++) count[u[k]] = c[k];
+  } else {
+    st = do_sync(ctx);
+    if (st) return st;
+  }
+  if (total) *total = ctx->hstatus->interactions;
+  return BH_OK;
+}
+
+bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out) {
+  if (!ctx || !out) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  if (st) return st;
+  out->n_records = ctx->hstatus->n_records;
+  out->n_internal = ctx->hstatus->n_internal;
+  out->node_capacity = ctx->lay.cap_rec;
+  out->interactions = (int64_t)ctx->hstatus->interactions;
+  out->mac_fallbacks = (int64_t)ctx->hstatus->fallbacks;
+  out->own_begin = ctx->own_lo;
+  out->own_end = ctx->own_hi;
+  out->steps = ctx->steps;
+  return BH_OK;
+}
+
+bh_status bh_set_profiling(bh_ctx *ctx, int enable) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  ctx->prof = enable != 0;
+  memset(ctx->prof_ms, 0, sizeof ctx->prof_ms);
+  memset(ctx->prof_launches, 0, sizeof ctx->prof_launches);
+  ctx->prof_calls = 0;
+  return st;
+}
+
+bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *calls) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  for (int i = 0; i < BH_NPHASE; i++) {
+    if (ms) ms[i] = ctx->prof_ms[i];
+    if (launches) launches[i] = ctx->prof_launches[i];
+  }
+  if (calls) *calls = ctx->prof_calls;
+  return st;
+}
+
+bh_status bh_nccl_unique_id(void *id128) {
+  if (!id128) return BH_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return BH_ERR_NCCL;
+  memcpy(id128, &id, sizeof id);
+  return BH_OK;
+}
+
+bh_status bh_nccl_comm_init(void **comm, const void *id128, int world, int rank, int device) {
+  if (!comm || !id128 || world < 1 || rank < 0 || rank >= world) return BH_ERR_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return BH_ERR_CUDA;
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  ncclComm_t c;
+  if (ncclCommInitRank(&c, world, id, rank) != ncclSuccess) return BH_ERR_NCCL;
+  *comm = (void *)c;
+  return BH_OK;
+}
+
+bh_status bh_nccl_comm_destroy(void *comm) {
+  if (!comm) return BH_OK;
+  return ncclCommDestroy((ncclComm_t)comm) == ncclSuccess ? BH_OK : BH_ERR_NCCL;
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// bh_internal.cuh -- shared definitions of the CUDA path (not part of the ABI).
+//
+// Data layout in HBM:
+//   storage order   : particles are relabelled once, at bh_create, by their
+//                     step-0 Morton rank ("storage id" s); rank r of P owns the
+//                     contiguous range [own_lo, own_hi).
+//   pos4[s]         : float4 (x, y, z, m), replicated on every rank.
+//   vel4[s-own_lo]  : float4 (vx, vy, vz, 0), this rank's particles only.
+//   uid[s]          : user index of storage id s.
+//   sorted arrays   : keys[p] (u64), vals[p] = s, lcp[p] (u8), nstart[p] (u32)
+//                     for Morton position p of the current step.
+//   walk records    : DFS pre-order array of tree nodes where every particle
+//                     has exactly one record (a single-particle leaf, or a
+//                     "member" record right after its level-21 bucket):
+//                       rec_cm[c]  float4 (com32.xyz, M32)       16 B
+//                       rec_aux[c] uint4  (T_acc, T_rej, skip, meta) 16 B
+//                       rec_first[c] u32 first sorted particle  (export)
+//                       rec_mom[c] double4 (M, MX, MY, MZ) fp64 (internal)
+//                     skip(c) = index of the first record after c's subtree,
+//                     so DFS next = c + 1 and "accept" jumps to skip(c).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bh.h"
+
+#define BH_MAXLEVEL 21
+#define BH_NPHASE 6
+
+namespace bh {
+
+// meta bits of rec_aux[c].w
+enum : uint32_t {
+  META_LEVEL_MASK = 0x1f,  // level 0..21; 22 for bucket members
+  META_LEAF = 1u << 5,     // single-particle leaf or bucket member (has no children)
+  META_MEMBER = 1u << 6,   // bucket member record (not a tree node of the export)
+  META_BUCKET = 1u << 7,   // level-21 node with >= 2 particles
+};
+
+// device status block (one per ctx, in the workspace)
+enum : uint32_t {
+  ERR_NONFINITE_POS = 1u << 0,
+  ERR_NONFINITE_FORCE = 1u << 1,
+  ERR_NODE_OVERFLOW = 1u << 2,
+};
+
+struct DevStatus {
+  uint32_t err;
+  uint32_t n_records;   // total walk records (nstart[n])
+  uint32_t n_internal;
+  uint32_t bbox_ticket; // last-block ticket of the bbox reduction
+  unsigned long long interactions;
+  unsigned long long fallbacks;
+  float lo[3];
+  float L;
+  float scale;
+  uint32_t pad[3];
+  uint32_t lvl_count[24];   // internal nodes per level (0..21)
+  uint32_t lvl_offset[24];  // exclusive prefix of lvl_count
+  uint32_t lvl_cursor[24];
+};
+
+struct Workspace {
+  float4 *pos4;
+  float4 *vel4;
+  uint32_t *uid;
+  unsigned long long *keys[2];
+  uint32_t *vals[2];
+  uint8_t *lcp;
+  uint32_t *nstart;   // n + 1
+  uint32_t *icount;   // interactions per storage id
+  float *accu;        // n * 3, user order (BH_HOST force output staging)
+  uint32_t *targets;  // own sorted positions (world > 1)
+  uint32_t *scan_tmp; // scan tile partials
+  uint32_t *sort_hist;    // 8 x 256
+  uint32_t *sort_status;  // 8 passes x tiles x 256
+  uint32_t *sort_tilectr; // 8
+  float *bbox_part;       // partial min/max per block (8 floats)
+  float4 *rec_cm;
+  uint4 *rec_aux;
+  uint32_t *rec_first;
+  double4 *rec_mom;
+  uint32_t *lvl_list;
+  DevStatus *status;
+};
+
+struct Layout {
+  int64_t n, cap_rec, cap_int, n_own_max, sort_tiles, scan_tiles;
+  size_t total;
+  size_t off[32];
+};
+
+// radix sort geometry (sort.cu)
+constexpr int SORT_BLOCK = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_BLOCK * SORT_ITEMS;
+constexpr int SORT_PASSES = 8;
+constexpr int SORT_RADIX = 256;
+
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
+
+constexpr int BBOX_BLOCKS = 592;  // 4 x 148 SMs
+
+Layout make_layout(int64_t n, int world, int64_t node_capacity);
+void bind_workspace(const Layout &L, void *base, Workspace &W);
+
+// ---- kernel launchers (each returns cudaGetLastError()) -------------------
+cudaError_t launch_bbox(const Workspace &W, int64_t n, cudaStream_t s);
+cudaError_t launch_keys(const Workspace &W, int64_t n, cudaStream_t s);
+cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *final_buf);
+cudaError_t launch_tie_fixup(const Workspace &W, int64_t n, int buf, cudaStream_t s);
+cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, cudaStream_t s);
+cudaError_t launch_moments(const Workspace &W, int64_t n, int64_t cap_rec, int64_t cap_int, double theta,
+                           cudaStream_t s, int *launches);
+cudaError_t launch_scan_u32(uint32_t *data, int64_t count, uint32_t *tmp, cudaStream_t s);
+cudaError_t launch_own_targets(const Workspace &W, int64_t n, int buf, uint32_t own_lo, uint32_t own_hi,
+                               cudaStream_t s);
+
+struct WalkArgs {
+  int64_t n;            // particles
+  int64_t n_targets;    // targets walked (own count)
+  int use_targets;      // 1: targets[] holds sorted positions; 0: target t is sorted position t
+  int buf;              // sort buffer holding vals
+  int group;            // lanes per shared traversal
+  int mode;             // 0 = forces to acc_out (user order), 1 = fused leapfrog
+  float eps2, G;
+  float kick, dt;       // mode 1
+  double theta2;
+  uint32_t own_lo;
+  float *acc_out;       // mode 0: user-order [n][3] device pointer (may be null)
+};
+cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s);
+
+}  // namespace bh

@@ -1,0 +1,114 @@
+// com.cu -- K5: level-synchronous bottom-up mass and centre of mass.
+//
+// PAPER.md:60-61 (§1): the octree is used "to compute center of mass and force
+// on each of the cubes"; Fig. 2 caption: P3 and P4 "may be
+// replaced by an equivalent centroid".  Reading L14: M and
+// MX = sum m x are fp64 sums over the children in Morton digit order, left to
+// right from 0 (bucket members in sorted order); a leaf contributes M = m,
+// MX = m x, exact in fp64 (24 x 24-bit products); com = MX / M.  Every fp64
+// operation is an explicit round-to-nearest intrinsic, so the result is
+// bit-identical to the oracle's recursive sums.
+//
+// One launch per level l = 21 .. 0 over that level's node list (K4 built the
+// lists); a node reads its children's records, which the previous launch (or
+// K4, for particle records) wrote.  The kernel also emits each node's fp32 walk
+// record: com32 = RN(com), M32 = RN(M), and the two fp32 thresholds of the
+// force walk's MAC filter (walk.cu):
+//   accept for sure  if d2_32 > T_acc,   open for sure  if d2_32 < T_rej,
+//   otherwise the walk re-evaluates the exact fp64 test of the oracle.
+// With r = s_l / theta the exact test is d > r (s^2 < theta^2 d^2).  The fp32
+// distance of the walk differs from the oracle's fp64 distance by at most
+//   |d32 - d| <= 2u d + 2u |c32|   (u = 2^-24: com rounding + subtraction)
+// and the fp32 sum of squares by a relative 8u; delta = 1e-12 covers the
+// oracle's own fp64 rounding.  Hence (safety factor 2 on every term)
+//   T_acc = RU(((r(1+delta) + b) / (1-a))^2 (1+g)),
+//   T_rej = RD(((r(1-delta) - b) / (1+a))^2 (1-g))   (or -inf if negative),
+// with a = 2u, b = 2u |c32| 1.001, g = 8u.  theta == 0: T_acc = T_rej = +inf.
+#include <math.h>
+
+#include "bh_internal.cuh"
+
+namespace bh {
+
+__device__ __forceinline__ float round_up_f(double x) {
+  float f = __double2float_ru(x);
+  return f;
+}
+__device__ __forceinline__ float round_down_f(double x) {
+  float f = __double2float_rd(x);
+  return f;
+}
+
+__global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatus *__restrict__ st,
+                                                       const uint32_t *__restrict__ lvl_list,
+                                                       float4 *__restrict__ rec_cm, uint4 *__restrict__ rec_aux,
+                                                       double4 *__restrict__ rec_mom, double theta) {
+  if (st->err & ERR_NODE_OVERFLOW) return;
+  const uint32_t cnt = st->lvl_count[level];
+  const uint32_t off = st->lvl_offset[level];
+  const double Ld = (double)st->L;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    const uint32_t c = lvl_list[off + t];
+    const uint4 aux = rec_aux[c];
+    const uint32_t end = aux.z;
+    double M = 0.0, X = 0.0, Y = 0.0, Z = 0.0;
+    uint32_t ch = c + 1;
+    while (ch < end) {
+      uint4 ca = rec_aux[ch];
+      if (ca.w & META_LEAF) {
+        float4 p = rec_cm[ch];
+        double m = (double)p.w;
+        M = __dadd_rn(M, m);
+        X = __dadd_rn(X, __dmul_rn(m, (double)p.x));
+        Y = __dadd_rn(Y, __dmul_rn(m, (double)p.y));
+        Z = __dadd_rn(Z, __dmul_rn(m, (double)p.z));
+        ch = ch + 1;
+      } else {
+        double4 q = rec_mom[ch];
+        M = __dadd_rn(M, q.x);
+        X = __dadd_rn(X, q.y);
+        Y = __dadd_rn(Y, q.z);
+        Z = __dadd_rn(Z, q.w);
+        ch = ca.z;
+      }
+    }
+    rec_mom[c] = make_double4(M, X, Y, Z);
+    const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
+    const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
+    rec_cm[c] = make_float4(fx, fy, fz, __double2float_rn(M));
+    float tacc, trej;
+    if (!(theta > 0.0)) {
+      tacc = INFINITY;
+      trej = INFINITY;
+    } else {
+      const double u = 5.9604644775390625e-08;  // 2^-24
+      const double s = ldexp(Ld, -level);
+      const double r = s / theta;
+      const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
+      const double a = 2.0 * u, b = 2.0 * u * C * 1.001, g = 8.0 * u, delta = 1e-12;
+      const double A = (r * (1.0 + delta) + b) / (1.0 - a);
+      tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15));
+      const double B = (r * (1.0 - delta) - b) / (1.0 + a);
+      trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 1e-15)) : -INFINITY;
+    }
+    rec_aux[c] = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), aux.z, aux.w);
+  }
+}
+
+cudaError_t launch_moments(const Workspace &W, int64_t n, int64_t cap_rec, int64_t cap_int, double theta,
+                           cudaStream_t s, int *launches) {
+  (void)cap_rec;
+  // grid: enough blocks for the widest level, capped at 8 waves of 148 SMs
+  int64_t need = (cap_int + 255) / 256;
+  if (n < 2) return cudaSuccess;
+  int64_t lim = 148 * 8;
+  int grid = (int)(need < lim ? need : lim);
+  if (grid < 1) grid = 1;
+  for (int l = BH_MAXLEVEL; l >= 0; l--) {
+    k_moments_level<<<grid, 256, 0, s>>>(l, W.status, W.lvl_list, W.rec_cm, W.rec_aux, W.rec_mom, theta);
+    if (launches) (*launches)++;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace bh

@@ -1,0 +1,230 @@
+// sort.cu -- K2: in-house LSD radix sort of (63-bit Morton key, u32 storage id).
+//
+// PAPER.md:58-60 builds the cube hierarchy with "a recursive algorithm"; on
+// B200 the hierarchy is read off the Morton-sorted key array instead, so the
+// sort is the tree build's dominant HBM stage.  Reading L13:
+// the order is ascending key, ties by ascending user index.
+//
+// Design (Onesweep, one kernel per 8-bit digit pass, 8 passes):
+//   * the 8 digit histograms come for free from K1 (keys.cu);
+//   * each CTA takes the next tile (4096 keys) from an atomic ticket, ranks its
+//     keys with warp-level match_any multisplit (stable within the tile),
+//     publishes per-digit tile counts and resolves its global offsets by
+//     decoupled look-back over earlier tiles (flag + 30-bit count in one
+//     32-bit word, so a single relaxed load/store carries both);
+//   * keys are reordered in shared memory by digit, then written out, so the
+//     stores are runs of consecutive addresses.
+// HBM roofline: per pass 12 B read + 12 B written per key -> 192 B/key over 8
+// passes.  Stability of LSD radix makes ties follow the input order; a tiny
+// fix-up pass re-sorts runs of equal keys by user index (runs are rare: they
+// are exact coincidences at the 2^-21 cell size).
+#include "bh_internal.cuh"
+
+namespace bh {
+
+constexpr int SORT_WARPS = SORT_BLOCK / 32;
+constexpr uint32_t FLAG_AGG = 1u << 30;
+constexpr uint32_t FLAG_PRE = 2u << 30;
+constexpr uint32_t VAL_MASK = (1u << 30) - 1;
+
+struct SortSmem {
+  unsigned long long keys[SORT_TILE];
+  uint32_t vals[SORT_TILE];
+  uint32_t wcount[SORT_WARPS][SORT_RADIX];
+  uint32_t dstart[SORT_RADIX];
+  int32_t gbase[SORT_RADIX];
+  uint32_t scan_tmp[SORT_WARPS * 2];
+  uint32_t tile;
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// exclusive block scan of one value per thread (SORT_BLOCK threads); returns
+// the exclusive prefix, *total receives the block total.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *tmp, uint32_t *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < SORT_WARPS ? tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < SORT_WARPS) tmp[SORT_WARPS + lane] = t;  // inclusive per warp
+  }
+  __syncthreads();
+  uint32_t warp_excl = w ? tmp[SORT_WARPS + w - 1] : 0;
+  *total = tmp[2 * SORT_WARPS - 1];
+  __syncthreads();
+  return warp_excl + x - v;
+}
+
+__global__ void __launch_bounds__(SORT_BLOCK) k_onesweep(const unsigned long long *__restrict__ kin,
+                                                         const uint32_t *__restrict__ vin,
+                                                         unsigned long long *__restrict__ kout,
+                                                         uint32_t *__restrict__ vout, int64_t n, int shift,
+                                                         const uint32_t *__restrict__ hist, uint32_t *status,
+                                                         uint32_t *tile_ctr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem &S = *reinterpret_cast<SortSmem *>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
+  for (int i = tid; i < SORT_WARPS * SORT_RADIX; i += SORT_BLOCK) (&S.wcount[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = S.tile;
+  const int64_t tbase = (int64_t)tile * SORT_TILE;
+  const int64_t wbase = tbase + (int64_t)warp * 32 * SORT_ITEMS;
+
+  unsigned long long k[SORT_ITEMS];
+  uint32_t v[SORT_ITEMS], rank[SORT_ITEMS];
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; j++) {
+    int64_t idx = wbase + j * 32 + lane;
+    if (idx < n) { k[j] = kin[idx]; v[j] = vin[idx]; }
+    else { k[j] = 0; v[j] = 0; }
+  }
+  // warp multisplit ranking, stable in (j, lane) order
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; j++) {
+    int64_t idx = wbase + j * 32 + lane;
+    bool valid = idx < n;
+    uint32_t act = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      uint32_t dig = (uint32_t)(k[j] >> shift) & 0xffu;
+      uint32_t peers = __match_any_sync(act, dig);
+      int leader = 31 - __clz(peers);
+      uint32_t below = __popc(peers & lanemask_lt());
+      uint32_t base = 0;
+      if (lane == leader) {
+        base = S.wcount[warp][dig];
+        S.wcount[warp][dig] = base + __popc(peers);
+      }
+      base = __shfl_sync(act, base, leader);
+      rank[j] = base + below;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit (thread == digit): exclusive offsets across warps, tile total
+  const int dd = tid;
+  uint32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < SORT_WARPS; w++) {
+    uint32_t c = S.wcount[w][dd];
+    S.wcount[w][dd] = tot;
+    tot += c;
+  }
+  uint32_t dummy;
+  uint32_t dstart = block_excl_scan(tot, S.scan_tmp, &dummy);
+  uint32_t gdig = block_excl_scan(hist[dd], S.scan_tmp, &dummy);
+  S.dstart[dd] = dstart;
+  // decoupled look-back for digit dd
+  uint32_t *my = status + (size_t)tile * SORT_RADIX + dd;
+  uint32_t excl = 0;
+  if (tile == 0) {
+    st_relaxed(my, FLAG_PRE | tot);
+  } else {
+    st_relaxed(my, FLAG_AGG | tot);
+    int64_t t = (int64_t)tile - 1;
+    for (;;) {
+      uint32_t s = ld_relaxed(status + (size_t)t * SORT_RADIX + dd);
+      uint32_t f = s & ~VAL_MASK;
+      if (f == 0) continue;
+      excl += s & VAL_MASK;
+      if (f == FLAG_PRE) break;
+      --t;
+    }
+    st_relaxed(my, FLAG_PRE | (excl + tot));
+  }
+  S.gbase[dd] = (int32_t)(gdig + excl) - (int32_t)dstart;
+  __syncthreads();
+  // scatter into shared memory in tile-sorted order
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; j++) {
+    int64_t idx = wbase + j * 32 + lane;
+    if (idx < n) {
+      uint32_t dig = (uint32_t)(k[j] >> shift) & 0xffu;
+      uint32_t loc = S.dstart[dig] + S.wcount[warp][dig] + rank[j];
+      S.keys[loc] = k[j];
+      S.vals[loc] = v[j];
+    }
+  }
+  __syncthreads();
+  int64_t rem = n - tbase;
+  const int valid_n = rem < SORT_TILE ? (int)rem : SORT_TILE;
+  for (int i = tid; i < valid_n; i += SORT_BLOCK) {
+    unsigned long long key = S.keys[i];
+    uint32_t dig = (uint32_t)(key >> shift) & 0xffu;
+    int64_t g = (int64_t)S.gbase[dig] + i;
+    kout[g] = key;
+    vout[g] = S.vals[i];
+  }
+}
+
+// ties: re-sort each run of equal keys by user index (insertion sort; runs are
+// rare and, after the first step, almost always already in order).
+__global__ void k_tie_fixup(const unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+                            const uint32_t *__restrict__ uid, int64_t n) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p + 1 >= n) return;
+  unsigned long long kp = keys[p];
+  if (keys[p + 1] != kp) return;
+  if (p > 0 && keys[p - 1] == kp) return;
+  int64_t e = p + 1;
+  while (e + 1 < n && keys[e + 1] == kp) ++e;
+  for (int64_t i = p + 1; i <= e; ++i) {
+    uint32_t v = vals[i];
+    uint32_t u = uid[v];
+    int64_t j = i - 1;
+    while (j >= p && uid[vals[j]] > u) { vals[j + 1] = vals[j]; --j; }
+    vals[j + 1] = v;
+  }
+}
+
+cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *final_buf) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+  int src = 0;
+  for (int pass = 0; pass < SORT_PASSES; pass++) {
+    k_onesweep<<<(unsigned)tiles, SORT_BLOCK, sizeof(SortSmem), s>>>(
+        W.keys[src], W.vals[src], W.keys[src ^ 1], W.vals[src ^ 1], n, 8 * pass, W.sort_hist + pass * SORT_RADIX,
+        W.sort_status + (size_t)pass * tiles * SORT_RADIX, W.sort_tilectr + pass);
+    src ^= 1;
+  }
+  *final_buf = src;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tie_fixup(const Workspace &W, int64_t n, int buf, cudaStream_t s) {
+  if (n < 2) return cudaSuccess;
+  k_tie_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.uid, n);
+  return cudaGetLastError();
+}
+
+}  // namespace bh

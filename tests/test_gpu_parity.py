@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bar (BASELINE.json north_star): Morton keys, sort permutation and tree topology
+bit-exact; fp64 moments bit-exact (reading L14); interaction counts
+integer-exact (the MAC decisions are exact); per-particle accelerations and
+positions after the stated steps within 1e-4 relative error,
+max_i |a_gpu - a_ref| / |a_ref| (reading L23).
+"""
+import numpy as np
+import pytest
+
+import bhgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def BH():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_1109_5190_b200 import BarnesHut
+
+    return BarnesHut
+
+
+def relerr(a, ref):
+    a = np.asarray(a, np.float64)
+    ref = np.asarray(ref, np.float64)
+    num = np.linalg.norm(a - ref, axis=1)
+    den = np.linalg.norm(ref, axis=1)
+    return np.where(den > 0, num / np.where(den > 0, den, 1), num)
+
+
+def _oracle(m, p, v, prm):
+    return oracle.Oracle(m, np.asarray(p, np.float64), None if v is None else np.asarray(v, np.float64), **prm).build()
+
+
+def check_step0(bh, o, n, full_forces=True, targets=None):
+    k, perm = bh.get_keys()
+    ok, operm = o.keys()
+    assert np.array_equal(k, ok), "Morton keys differ"
+    assert np.array_equal(perm.astype(np.int64), operm), "sort permutation differs"
+    lv, fi, co = bh.get_tree()
+    olv, ofi, oco, oM, oMX = o.tree(with_moments=True)
+    assert len(lv) == len(olv), f"node count {len(lv)} vs {len(olv)}"
+    assert np.array_equal(lv, olv) and np.array_equal(fi, ofi) and np.array_equal(co, oco), "topology differs"
+    M, MX = bh.get_moments()
+    assert np.array_equal(M, oM) and np.array_equal(MX, oMX), "fp64 moments not bit-identical"
+    acc = bh.compute_forces()
+    cnt, total = bh.get_interactions()
+    if targets is None:
+        oacc, ocnt = o.forces()
+        assert np.array_equal(cnt.astype(np.int64), ocnt), "interaction counts differ"
+        assert total == int(ocnt.sum())
+        err = relerr(acc, oacc)
+    else:
+        oacc, ocnt = o.forces(targets)
+        assert np.array_equal(cnt[targets].astype(np.int64), ocnt), "interaction counts differ"
+        err = relerr(acc[targets], oacc)
+    assert err.max() < TOL, f"acceleration max rel err {err.max():.3e}"
+    return acc, err
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_full_config_parity_free_running(BH, cfg):
+    """cfg1 (1 step) and cfg2 (10 steps): step 0 bit-exact + forces, then the
+    free-running trajectory (positions <= 1e-4 after the stated steps) and a
+    teacher-forced check on the GPU's final state (reading L24)."""
+    c = bhgen.CONFIGS[cfg]
+    m, p, v = bhgen.generate(cfg)
+    prm = bhgen.params(cfg)
+    bh = BH(m, p, v, **prm)
+    bh.build_tree()
+    o = _oracle(m, p, v, prm)
+    check_step0(bh, o, c.n)
+    bh.step(c.steps)
+    gpos, gvel = bh.get_state()
+    o.step(c.steps)
+    opos, ovel = o.state()
+    perr = relerr(gpos, opos)
+    assert perr.max() < TOL, f"positions after {c.steps} steps: {perr.max():.3e}"
+    # teacher-forced: the oracle on the GPU's fp32 state reproduces keys/topology/forces
+    bh.build_tree()
+    ot = oracle.Oracle(m, gpos.astype(np.float64), gvel.astype(np.float64), **prm).build()
+    check_step0(bh, ot, c.n)
+    st = bh.get_stats()
+    assert st["steps"] == c.steps
+
+
+def test_cfg3_full_step0_and_one_step(BH):
+    m, p, v = bhgen.generate("cfg3")
+    prm = bhgen.params("cfg3")
+    bh = BH(m, p, v, **prm)
+    bh.build_tree()
+    o = _oracle(m, p, v, prm)
+    check_step0(bh, o, m.shape[0])
+    bh.step(2)
+    o.step(2)
+    gpos, _ = bh.get_state()
+    opos, _ = o.state()
+    assert relerr(gpos, opos).max() < TOL
+
+
+@pytest.mark.parametrize("cfg", ["cfg4"])
+def test_full_size_sampled(BH, cfg):
+    """BASELINE full size (N = 2^24) in the bench's launch configuration:
+    keys / permutation / topology bit-exact over all N, forces on 2048 sampled
+    targets, counts integer-exact."""
+    m, p, v = bhgen.generate(cfg)
+    prm = bhgen.params(cfg)
+    bh = BH(m, p, v, **prm)
+    bh.build_tree()
+    o = _oracle(m, p, v, prm)
+    rng = np.random.default_rng(7)
+    targets = np.sort(rng.choice(m.shape[0], 2048, replace=False))
+    check_step0(bh, o, m.shape[0], targets=targets)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 4097, 5000])
+def test_ragged_and_tiny_sizes(BH, n):
+    m, p, v = bhgen.generate("cfg2", n=n)
+    prm = bhgen.params("cfg2")
+    bh = BH(m, p, v, **prm)
+    bh.build_tree()
+    o = _oracle(m, p, v, prm)
+    if n == 1:
+        a = bh.compute_forces()
+        assert np.all(a == 0)
+        k, perm = bh.get_keys()
+        assert list(perm) == [0]
+        return
+    check_step0(bh, o, n)
+    bh.step(3)
+    o.step(3)
+    assert relerr(bh.get_state()[0], o.state()[0]).max() < TOL
+
+
+def test_buckets_duplicates_coincident(BH):
+    rng = np.random.default_rng(1)
+    base = rng.random((3000, 3)).astype(np.float32)
+    pos = np.vstack([base, base[rng.integers(0, 3000, 200)], np.tile(base[:1], (40, 1))])
+    pos = pos[rng.permutation(pos.shape[0])]
+    n = pos.shape[0]
+    m = (rng.random(n) + 0.5).astype(np.float32)
+    prm = dict(theta=0.6, eps=1e-2, G=1.0, dt=1e-3)
+    bh = BH(m, pos, None, **prm)
+    bh.build_tree()
+    o = _oracle(m, pos, None, prm)
+    check_step0(bh, o, n)
+    lv, fi, co = bh.get_tree()
+    assert np.any((lv == 21) & (co >= 2)), "expected level-21 buckets"
+    # all particles coincident: L = 0, 22-node chain ending in a bucket
+    pos = np.tile(np.float32([[0.5, -1.0, 2.0]]), (1000, 1))
+    bh = BH(np.ones(1000, np.float32), pos, None, **prm)
+    bh.build_tree()
+    lv, fi, co = bh.get_tree()
+    assert list(lv) == list(range(22)) and np.all(co == 1000)
+    a = bh.compute_forces()
+    assert np.all(a == 0)
+    cnt, _ = bh.get_interactions()
+    assert np.all(cnt == 999)
+
+
+def test_faces_and_theta0_direct(BH):
+    rng = np.random.default_rng(2)
+    pos = (rng.integers(0, 5, size=(2000, 3)) * 0.25).astype(np.float32) + rng.random((2000, 3)).astype(np.float32) * 1e-3
+    pos[:10] = np.float32([[0, 0, 0]]) + 0  # on the lower faces
+    m = np.full(2000, 1 / 2000, np.float32)
+    prm = dict(theta=0.0, eps=1e-3, G=1.0, dt=1e-3)
+    bh = BH(m, pos, None, **prm)
+    bh.build_tree()
+    o = _oracle(m, pos, None, prm)
+    acc, _ = check_step0(bh, o, 2000)
+    cnt, _ = bh.get_interactions()
+    ref = oracle.direct(m, pos, 1e-3)
+    assert relerr(acc, ref).max() < TOL and np.all(cnt == 1999)
+
+
+def test_errors(BH):
+    from paper_1109_5190_b200 import BhError
+
+    m = np.ones(4, np.float32)
+    pos = np.float32([[0, 0, 0], [1, 0, 0], [1, 0, 0], [0, 1, 0]])
+    bh = BH(m, pos, None, theta=0.5, eps=0.0)
+    with pytest.raises(BhError) as e:
+        bh.compute_forces()  # before bh_build_tree
+    assert e.value.code == -4
+    bh.build_tree()
+    with pytest.raises(BhError) as e:
+        bh.compute_forces()  # eps == 0 and coincident pair
+    assert e.value.code == -5
+    bad = pos.copy()
+    bad[2, 1] = np.nan
+    with pytest.raises(BhError) as e:
+        BH(m, bad, None, theta=0.5, eps=0.1)
+    assert e.value.code == -5
+    with pytest.raises(BhError) as e:
+        BH(m, pos, None, theta=-1.0, eps=0.1)
+    assert e.value.code == -1
+    # node capacity too small for the tree -> BH_ERR_OOM
+    mm, pp, _ = bhgen.generate("cfg1")
+    bh = BH(mm, pp, None, theta=0.5, eps=1e-3, node_capacity=4097)
+    bh.build_tree()
+    with pytest.raises(BhError) as e:
+        bh.sync()
+    assert e.value.code == -3
+
+
+@pytest.mark.parametrize("group", [1, 4, 16])
+def test_walk_group_invariance(BH, group):
+    """The traversal-sharing group size changes nothing: bitwise equal forces."""
+    m, p, v = bhgen.generate("cfg2", n=20000)
+    prm = bhgen.params("cfg2")
+    a = BH(m, p, v, **prm)
+    a.build_tree()
+    ref = a.compute_forces()
+    b = BH(m, p, v, walk_group=group, **prm)
+    b.build_tree()
+    got = b.compute_forces()
+    assert np.array_equal(got, ref)
+    assert np.array_equal(a.get_interactions()[0], b.get_interactions()[0])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_emulation_bitwise(BH, world):
+    """Multi-GPU path emulated on one GPU (no NCCL): each rank's walk over its
+    owned Morton range gives bitwise the P = 1 forces and one-step positions."""
+    m, p, v = bhgen.generate("cfg2", n=30000)
+    prm = bhgen.params("cfg2")
+    one = BH(m, p, v, **prm)
+    one.build_tree()
+    ref = one.compute_forces()
+    one.step(1)
+    ref_pos, ref_vel = one.get_state()
+    got = np.full_like(ref, np.nan)
+    got_pos = np.full_like(ref, np.nan)
+    got_vel = np.full_like(ref, np.nan)
+    for r in range(world):
+        bh = BH(m, p, v, rank=r, world=world, **prm)
+        st = bh.get_stats()
+        lo, hi = st["own_begin"], st["own_end"]
+        assert hi > lo
+        bh.build_tree()
+        # storage order == step-0 Morton order, so the owned users are perm[lo:hi]
+        _, perm = bh.get_keys()
+        own = perm[lo:hi].astype(np.int64)
+        a = bh.compute_forces()
+        got[own] = a[own]
+        bh.step(1)
+        pos, vel = bh.get_state()
+        got_pos[own] = pos[own]
+        got_vel[own] = vel[own]
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref)
+    assert np.array_equal(got_pos, ref_pos) and np.array_equal(got_vel, ref_vel)
+
+
+def test_device_pointer_paths(BH):
+    import torch
+
+    m, p, v = bhgen.generate("cfg1")
+    prm = bhgen.params("cfg1")
+    dm, dp, dv = (torch.from_numpy(x).cuda() for x in (m, p, v))
+    bh = BH(dm, dp, dv, **prm)
+    bh.build_tree()
+    out = torch.empty((m.shape[0], 3), dtype=torch.float32, device="cuda")
+    bh.compute_forces(out)
+    host = BH(m, p, v, **prm)
+    host.build_tree()
+    assert np.array_equal(out.cpu().numpy(), host.compute_forces())
+    bh.step(1)
+    po = torch.empty_like(out)
+    vo = torch.empty_like(out)
+    bh.get_state(po, vo)
+    host.step(1)
+    hp, hv = host.get_state()
+    assert np.array_equal(po.cpu().numpy(), hp) and np.array_equal(vo.cpu().numpy(), hv)
+    bh.set_state(dm, dp, dv)
+    bh.step(1)
+    bh.get_state(po, vo)
+    assert np.array_equal(po.cpu().numpy(), hp)
+
+
+def test_sort_vs_lexsort_many_ties(BH):
+    """K2 + tie fix-up == numpy lexsort (library routine) on heavy ties, over
+    several steps (ties recur in storage order != user order)."""
+    rng = np.random.default_rng(9)
+    pos = rng.integers(0, 16, size=(50000, 3)).astype(np.float32)
+    vel = rng.normal(size=(50000, 3)).astype(np.float32)
+    m = np.ones(50000, np.float32)
+    bh = BH(m, pos, vel, theta=0.5, eps=0.5, dt=1e-9)
+    for step in range(3):
+        bh.build_tree()
+        k, perm = bh.get_keys()
+        gpos, _ = bh.get_state()
+        o = oracle.Oracle(m, gpos.astype(np.float64), None, theta=0.5, eps=0.5).build()
+        ok, operm = o.keys()
+        assert np.array_equal(k, ok) and np.array_equal(perm.astype(np.int64), operm)
+        user_keys = np.empty_like(ok)
+        user_keys[operm] = ok
+        assert np.array_equal(operm, np.lexsort((np.arange(50000), user_keys)))
+        bh.step(1)
