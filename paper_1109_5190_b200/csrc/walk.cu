@@ -57,7 +57,7 @@ struct WalkParams {
 
 __device__ __noinline__ bool exact_accept(const double4 *__restrict__ rec_mom, uint32_t c, uint32_t level, float x,
                                           float y, float z, double L, double theta2) {
-  // the oracle's fp64 test, operation for operation (oracle/bh_oracle.c mac_accept)
+  // the oracle's fp64 test (DESIGN.md §3 L4), operation for operation
   double4 m = rec_mom[c];
   double cx = __ddiv_rn(m.y, m.x), cy = __ddiv_rn(m.z, m.x), cz = __ddiv_rn(m.w, m.x);
   double dx = __dsub_rn(cx, (double)x), dy = __dsub_rn(cy, (double)y), dz = __dsub_rn(cz, (double)z);
