@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Barnes-Hut step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+A "step" is one bh_step: the whole hot path (K0 root cube, K1 keys, K2 radix
+sort, K4 octree, K5 moments, K6+K7 walk + leapfrog, K8 exchange when N > 1) over
+the full particle set.  Default workload: BASELINE cfg4 (N = 2^24 Plummer,
+theta = 0.5, eps = 1e-3, dt = 1e-4), the largest configuration that fits one GPU
+and the one the 1/2/4/8-GPU metric is quoted on.  Inputs (pos4 268 MB, tree
+records ~1.1 GB) are larger than the 126 MB L2, so no flush is needed.
+
+`value` = total Barnes-Hut interactions of the K timed steps over all ranks /
+max-over-ranks device time (CUDA events on the library stream), i.e. whole-job
+interactions/s; particles/s is reported beside it.  For N > 1 the script runs
+under torchrun, one rank per GPU, NCCL over NVLink (strong scaling: N fixed).
+
+`--impl reference` times the plain fp64 CPU oracle (oracle/, the parity
+reference) on the box's host cores on a bounded sample of the same workload;
+it is the slow reference arm, not a target.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import bhgen  # noqa: E402
+
+METRIC = "BH interactions/s and particles/s per step at 1/2/4/8 B200; % FP32 peak"
+UNIT = "interactions/s"
+FLOP_PER_INTERACTION = 18  # dx,dy,dz 3 + d2 5 + r2 1 + rsqrt^3 2 + M* 1 + acc 6 (rsqrt itself not counted)
+FLOP_PER_OPEN = 8          # the MAC distance of a node that is opened: 3 sub + 5
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def fp32_peak_tflops(sm_count: int, mhz: float) -> float:
+    # 128 FP32 lanes per SM, FFMA = 2 flop (B200_PROFILING.md: 148 SMs, 1965 MHz max)
+    return 2.0 * 128 * sm_count * mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        loaded = [r[0] for r in rows if r[0] > 600] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def load_traffic(kernel_key: str, workload: str):
+    """dram bytes per launch of the walk from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        k = d["kernels"][kernel_key]
+        if d.get("workload") != workload:
+            return None, None
+        return k.get("dram_bytes_per_launch"), os.path.relpath(path, ROOT)
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
+# --------------------------------------------------------------------- oracle arm
+def run_oracle_sample(cfg, m, p, v, samples: int, reps: int, warm: int):
+    """Time the fp64 oracle as it stands: one full tree build, then `reps` walks
+    of `samples` random targets.  Returns a dict of rates."""
+    import oracle
+
+    n = m.shape[0]
+    prm = bhgen.params(cfg)
+    t0 = time.perf_counter()
+    o = oracle.Oracle(m, p.astype(np.float64), v.astype(np.float64), **prm)
+    o.build()
+    t_build = time.perf_counter() - t0
+    rng = np.random.default_rng(12345)
+    walk_t, inter = [], []
+    for r in range(warm + reps):
+        tg = rng.choice(n, min(samples, n), replace=False)
+        t1 = time.perf_counter()
+        _, cnt = o.forces(tg)
+        dt = time.perf_counter() - t1
+        if r >= warm:
+            walk_t.append(dt)
+            inter.append(int(cnt.sum()))
+    o.close()
+    s_tot = min(samples, n) * reps
+    walk_rate = sum(inter) / sum(walk_t)  # interactions/s of the walk alone
+    mean_i = sum(inter) / s_tot
+    # one whole step extrapolated: full build + all-particle walk at the sampled rate
+    t_step = t_build + n * mean_i / walk_rate
+    return {"interactions_per_s": n * mean_i / t_step, "particles_per_s": n / t_step, "t_build_s": t_build,
+            "walk_interactions_per_s": walk_rate, "mean_interactions": mean_i, "t_step_extrapolated_s": t_step,
+            "cores": len(os.sched_getaffinity(0)), "samples": min(samples, n), "reps": reps,
+            "step_times": walk_t}
+
+
+def reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0  # only rank 0 runs the CPU reference
+    cfg = bhgen.CONFIGS[args.config]
+    m, p, v = bhgen.generate(cfg)
+    samples = args.ref_samples
+    r = run_oracle_sample(cfg, m, p, v, samples, args.steps, args.warmup)
+    val = r["interactions_per_s"]
+    sample_desc = (f"full fp64 oracle tree build of all N={cfg.n} ({r['t_build_s']:.1f} s) + {args.steps} timed "
+                   f"walks of {r['samples']} random targets each ({args.warmup} warm-up); whole-step rate "
+                   f"extrapolated per particle")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["t_step_extrapolated_s"] * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(cfg, m, p, v),
+        "particles_per_s": r["particles_per_s"],
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": sample_desc,
+                         "walk_interactions_per_s": r["walk_interactions_per_s"], "t_build_s": r["t_build_s"]},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def workload_config(cfg, m, p, v):
+    return {"workload": f"{cfg.name}: N={cfg.n} {cfg.kind}, theta={cfg.theta}, eps={cfg.eps}, dt={cfg.dt}, G={cfg.G}",
+            "n": cfg.n, "theta": cfg.theta, "eps": cfg.eps, "dt": cfg.dt, "seed": cfg.seed,
+            "input_sha256": bhgen.digest(m, p, v)[:16],
+            "l2": "inputs larger than L2 (pos4 16 B x N, tree records ~50 B x 1.5 N); no flush"}
+
+
+# --------------------------------------------------------------------- our arm
+def ours_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1109_5190_b200 import BarnesHut, bh as bhmod
+
+    rank, world, local = env_rank()
+    if world != args.gpus and not (world == 1 and args.gpus == 1):
+        print(f"--gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    device = local if world > 1 else 0
+    torch.cuda.set_device(device)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
+        uid = [bhmod.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = bhmod.nccl_comm_init(uid[0], world, rank, device)
+    cfg = bhgen.CONFIGS[args.config]
+    m, p, v = bhgen.generate(cfg)
+    prm = bhgen.params(cfg)
+    bh = BarnesHut(m, p, v, device=device, rank=rank, world=world, nccl_comm=comm, walk_group=args.walk_group,
+                   **prm)
+    stream = bh.stream
+    props = torch.cuda.get_device_properties(device)
+    sms = props.multi_processor_count
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allreduce(x, op):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    # warm-up (untimed)
+    bh.step(args.warmup)
+    bh.sync()
+    st0 = bh.get_stats()
+    bh.set_profiling(True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            bh.step(1)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_local = ev0.elapsed_time(ev1)
+    prof = bh.get_profile()
+    st1 = bh.get_stats()
+    bh.set_profiling(False)
+    ms = allreduce(ms_local, dist.ReduceOp.MAX if world > 1 else None)
+    inter_local = st1["interactions_cum"] - st0["interactions_cum"]
+    opens_local = st1["opens_cum"] - st0["opens_cum"]
+    inter = allreduce(float(inter_local), dist.ReduceOp.SUM if world > 1 else None)
+    opens = allreduce(float(opens_local), dist.ReduceOp.SUM if world > 1 else None)
+    secs = ms / 1e3
+    value = inter / secs
+    particles_per_s = cfg.n * args.steps / secs
+
+    # roofline of the dominant kernel (the walk), measured live with CUDA events
+    walk_ms = prof["ms"]["walk"] / args.steps
+    flops_walk_launch = (FLOP_PER_INTERACTION * inter_local + FLOP_PER_OPEN * opens_local) / args.steps
+    achieved_tf = flops_walk_launch / (walk_ms / 1e3) / 1e12
+    peaks = measured_peaks()
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    peak = fp32_peak_tflops(sms, sm_max)
+    clocks = clk.summary()
+    traffic, traffic_src = load_traffic("walk", f"{cfg.name}")
+    phase_ms = {k: vv / args.steps for k, vv in prof["ms"].items()}
+    sort_bytes = 8 * 24 * cfg.n  # 8 passes x (8 B key + 4 B id) read + written
+    sort_gbs = sort_bytes / (phase_ms["sort"] / 1e3) / 1e9 if phase_ms["sort"] > 0 else None
+    launches = sum(prof["launches"].values())
+
+    # e2e: through the public API with host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+        hm, hp, hv = pin(m), pin(p), pin(v)
+        op = torch.empty((cfg.n, 3), dtype=torch.float32).pin_memory().numpy()
+        ov = torch.empty((cfg.n, 3), dtype=torch.float32).pin_memory().numpy()
+        bh.set_state(hm, hp, hv)
+        bh.step(1)
+        bh.get_state()  # warm the path
+        e_steps = max(1, min(args.steps, 5))
+        barrier()
+        torch.cuda.synchronize()
+        s0 = bh.get_stats()["interactions_cum"]
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            bh.set_state(hm, hp, hv)
+            bh.step(1)
+            bh.L.bh_get_state(bh.h, bhmod._ptr(op), bhmod._ptr(ov), bhmod.BH_HOST)
+        torch.cuda.synchronize()
+        t_e = allreduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None)
+        e_inter = allreduce(float(bh.get_stats()["interactions_cum"] - s0), dist.ReduceOp.SUM if world > 1 else None)
+        e2e = {"value": e_inter / t_e, "unit": UNIT, "h2d_bytes_per_step": int(cfg.n * (4 + 12 + 12)),
+               "d2h_bytes_per_step": int(cfg.n * (12 + 12)), "steps": e_steps,
+               "ms_per_step": t_e / e_steps * 1e3,
+               "path": "bh_set_state(pinned host) + bh_step(1) + bh_get_state(pinned host) per step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = run_oracle_sample(cfg, m, p, v, args.cpu_samples, 1, 0)
+        cpu = {"value": r["interactions_per_s"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+               "sample": (f"fp64 oracle: full tree build of N={cfg.n} ({r['t_build_s']:.1f} s) + walk of "
+                          f"{r['samples']} random targets; whole-step rate extrapolated per particle"),
+               "walk_interactions_per_s": r["walk_interactions_per_s"]}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": dict(workload_config(cfg, m, p, v), parallelism=f"morton-range x{world}",
+                           walk_group=args.walk_group or 32),
+            "particles_per_s": particles_per_s,
+            "interactions_per_step": inter / args.steps,
+            "fp32_peak_frac": achieved_tf / peak,
+            "roofline": {"bound": "alu", "kernel": "k_walk (K6+K7)", "achieved": achieved_tf, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved_tf / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "peak_source": f"derived: 2 flop x 128 FP32 lanes x {sms} SMs x {sm_max:.0f} MHz "
+                                        "(sm_max_mhz of MEASURED_PEAKS.json; B200_PROFILING.md)",
+                         "flops_per_launch": flops_walk_launch, "launch_ms": walk_ms,
+                         "flop_model": "18 per interaction + 8 per opened node"},
+            "hbm_stages": {"sort_GBps": sort_gbs, "sort_bytes_model": "8 passes x 24 B/particle",
+                           "hbm_peak_GBps": peaks.get("hbm_gbs")},
+            "phase_ms_per_step": phase_ms,
+            "mac_fallbacks_last_step": st1["mac_fallbacks"],
+            "tree_records": st1["n_records"],
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    bh.close()
+    if comm is not None:
+        bhmod.nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=sorted(bhgen.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--walk-group", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=20000)
+    ap.add_argument("--ref-samples", type=int, default=8192)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warm-up < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

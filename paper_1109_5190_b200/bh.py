@@ -54,6 +54,9 @@ class BhStats(C.Structure):
         ("own_begin", C.c_int64),
         ("own_end", C.c_int64),
         ("steps", C.c_int64),
+        ("opens", C.c_int64),
+        ("interactions_cum", C.c_int64),
+        ("opens_cum", C.c_int64),
     ]
 
 

@@ -351,7 +351,7 @@ static bh_status build_tree(bh_ctx *ctx) {
   return BH_OK;
 }
 
-static bh_status walk(bh_ctx *ctx, int mode, float kick) {
+static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool user_order) {
   const int64_t n = ctx->p.n;
   cudaStream_t s = ctx->stream;
   ProfPair pp;
@@ -369,8 +369,9 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick) {
   a.dt = (float)ctx->p.dt;
   a.theta2 = ctx->p.theta * ctx->p.theta;
   a.own_lo = (uint32_t)ctx->own_lo;
-  a.acc_out = mode == 0 ? ctx->W.accu : nullptr;
-  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 2 * sizeof(unsigned long long), s));
+  a.acc_out = mode == 0 ? acc_out : nullptr;
+  a.user_order = user_order ? 1 : 0;
+  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 3 * sizeof(unsigned long long), s));
   if (ctx->p.world > 1) {
     CK(launch_own_targets(ctx->W, n, ctx->sort_buf, (uint32_t)ctx->own_lo, (uint32_t)ctx->own_hi, s));
     a.use_targets = 1;
@@ -549,6 +550,7 @@ bh_status bh_set_state(bh_ctx *ctx, const float *mass, const float *pos, const f
                                                         ctx->own_lo, ctx->own_hi);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(&ctx->W.status->err, 0, sizeof(uint32_t), ctx->stream));
+  CK(cudaMemsetAsync(&ctx->W.status->interactions_cum, 0, 2 * sizeof(unsigned long long), ctx->stream));
   ctx->steps = 0;
   ctx->tree_valid = false;
   return BH_OK;
@@ -569,29 +571,30 @@ bh_status bh_compute_forces(bh_ctx *ctx, float *acc, int where) {
   if (!ctx->tree_valid) return fail(ctx, BH_ERR_STATE, "bh_compute_forces needs bh_build_tree on the current state");
   bh_status st = set_dev(ctx);
   if (st) return st;
-  st = walk(ctx, 0, 0.f);
-  if (st) return st;
   const int64_t lo = ctx->own_lo, hi = ctx->own_hi, own_n = hi - lo;
-  if (acc && where == BH_DEVICE) {
-    k_scatter3<<<blocks_for(own_n), 256, 0, ctx->stream>>>(acc, nullptr, ctx->W.accu, ctx->W.uid, lo, hi, 1);
-    CK(cudaGetLastError());
-    return enqueue_status(ctx);
+  const bool host_scatter = acc && where == BH_HOST && ctx->p.world > 1;
+  // device destination: the walk writes user order directly; host + one rank:
+  // user order into accu then one copy; host + several ranks: storage order + host scatter
+  float *dst = !acc ? nullptr : (where == BH_DEVICE ? acc : ctx->W.accu);
+  st = walk(ctx, 0, 0.f, dst, !host_scatter);
+  if (st) return st;
+  if (!acc) return enqueue_status(ctx);
+  if (where == BH_DEVICE) return enqueue_status(ctx);
+  if (!host_scatter) {
+    CK(cudaMemcpyAsync(acc, ctx->W.accu, (size_t)ctx->p.n * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    return do_sync(ctx);
   }
-  if (acc) {
-    // storage-order own slice + uid slice to host, scatter on the host
-    std::vector<float> a((size_t)own_n * 3);
-    std::vector<uint32_t> u((size_t)own_n);
-    CK(cudaMemcpyAsync(a.data(), ctx->W.accu, (size_t)own_n * 12, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(u.data(), ctx->W.uid + lo, (size_t)own_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    st = do_sync(ctx);
-    if (st) return st;
-    for (int64_t k = 0; k < own_n; k++) {
-      size_t ui = u[k];
-      acc[3 * ui] = a[3 * k]; acc[3 * ui + 1] = a[3 * k + 1]; acc[3 * ui + 2] = a[3 * k + 2];
-    }
-    return BH_OK;
+  std::vector<float> a((size_t)own_n * 3);
+  std::vector<uint32_t> u((size_t)own_n);
+  CK(cudaMemcpyAsync(a.data(), ctx->W.accu, (size_t)own_n * 12, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(u.data(), ctx->W.uid + lo, (size_t)own_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  st = do_sync(ctx);
+  if (st) return st;
+  for (int64_t k = 0; k < own_n; k++) {
+    size_t ui = u[k];
+    acc[3 * ui] = a[3 * k]; acc[3 * ui + 1] = a[3 * k + 1]; acc[3 * ui + 2] = a[3 * k + 2];
   }
-  return enqueue_status(ctx);
+  return BH_OK;
 }
 
 bh_status bh_step(bh_ctx *ctx, int nsteps) {
@@ -608,7 +611,7 @@ bh_status bh_step(bh_ctx *ctx, int nsteps) {
     st = build_tree(ctx);
     if (st) return st;
     float kick = (float)(ctx->steps == 0 ? 0.5 * ctx->p.dt : ctx->p.dt);
-    st = walk(ctx, 1, kick);
+    st = walk(ctx, 1, kick, nullptr, false);
     if (st) return st;
     st = exchange(ctx);
     if (st) return st;
@@ -654,6 +657,11 @@ bh_status bh_get_state(bh_ctx *ctx, float *pos, float *vel, int where) {
     if (where == BH_DEVICE) {
       k_scatter3<<<blocks_for(own_n), 256, 0, s>>>(vel, ctx->W.vel4, nullptr, ctx->W.uid, lo, hi, 1);
       CK(cudaGetLastError());
+    } else if (ctx->p.world == 1) {
+      float *tmp = ctx->W.accu;  // stream order: the position copy above has finished reading it
+      k_scatter3<<<blocks_for(own_n), 256, 0, s>>>(tmp, ctx->W.vel4, nullptr, ctx->W.uid, lo, hi, 1);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(vel, tmp, (size_t)n * 12, cudaMemcpyDeviceToHost, s));
     } else {
       std::vector<float4> v((size_t)own_n);
       std::vector<uint32_t> u((size_t)own_n);
@@ -795,6 +803,9 @@ bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out) {
   out->node_capacity = ctx->lay.cap_rec;
   out->interactions = (int64_t)ctx->hstatus->interactions;
   out->mac_fallbacks = (int64_t)ctx->hstatus->fallbacks;
+  out->opens = (int64_t)ctx->hstatus->opens;
+  out->interactions_cum = (int64_t)ctx->hstatus->interactions_cum;
+  out->opens_cum = (int64_t)ctx->hstatus->opens_cum;
   out->own_begin = ctx->own_lo;
   out->own_end = ctx->own_hi;
   out->steps = ctx->steps;

@@ -49,8 +49,12 @@ struct DevStatus {
   uint32_t n_records;   // total walk records (nstart[n])
   uint32_t n_internal;
   uint32_t bbox_ticket; // last-block ticket of the bbox reduction
-  unsigned long long interactions;
-  unsigned long long fallbacks;
+  unsigned long long interactions;   // last walk
+  unsigned long long fallbacks;      // last walk: fp64 MAC re-evaluations
+  unsigned long long opens;          // last walk: MAC tests that opened a node (incl. self leaf)
+  unsigned long long pad64;
+  unsigned long long interactions_cum;  // since create / set_state
+  unsigned long long opens_cum;
   float lo[3];
   float L;
   float scale;
@@ -129,7 +133,8 @@ struct WalkArgs {
   float kick, dt;       // mode 1
   double theta2;
   uint32_t own_lo;
-  float *acc_out;       // mode 0: user-order [n][3] device pointer (may be null)
+  float *acc_out;       // mode 0: [n][3] device output (may be null)
+  int user_order;       // 1: acc_out[uid[s]], 0: acc_out[s - own_lo]
 };
 cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s);
 

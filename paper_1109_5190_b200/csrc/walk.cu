@@ -46,7 +46,8 @@ struct WalkParams {
   uint32_t *icount;
   float4 *pos4;
   float4 *vel4;
-  float *acc_st;  // mode 0: storage-order own slice [(s - own_lo) * 3]
+  float *acc_out;  // mode 0: acc_out[3 uid[s]] (user_order) or acc_out[3 (s - own_lo)]
+  int user_order;
   int64_t n_targets;
   int use_targets;
   int mode;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   }
   const bool gvalid = (__ballot_sync(full, tvalid) & gmask) != 0u;
   uint32_t c = gvalid ? 0u : Wn;
-  uint32_t resume = 0, cnt = 0, fb = 0;
+  uint32_t resume = 0, cnt = 0, fb = 0, nop = 0;
   int bad = 0;
   float ax = 0.f, ay = 0.f, az = 0.f;
   double dax = 0.0, day = 0.0, daz = 0.0;
@@ -130,20 +131,23 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
       }
     }
     const bool opn = act && !acc;
+    nop += opn;
     const uint32_t ob = __ballot_sync(full, opn);
     if (live) c = (ob & gmask) ? c + 1u : skip;
   }
   dax += ax; day += ay; daz += az;
   // warp reductions of the counters
-  unsigned long long wc = cnt, wf = fb;
+  unsigned long long wc = cnt, wf = fb, wo = nop;
   for (int o = 16; o; o >>= 1) {
     wc += __shfl_xor_sync(full, wc, o);
     wf += __shfl_xor_sync(full, wf, o);
+    wo += __shfl_xor_sync(full, wo, o);
   }
   const int wbad = __any_sync(full, bad);
   if (lane == 0) {
-    if (wc) atomicAdd(&P.st->interactions, wc);
+    if (wc) { atomicAdd(&P.st->interactions, wc); atomicAdd(&P.st->interactions_cum, wc); }
     if (wf) atomicAdd(&P.st->fallbacks, wf);
+    if (wo) { atomicAdd(&P.st->opens, wo); atomicAdd(&P.st->opens_cum, wo); }
     if (wbad) atomicOr(&P.st->err, ERR_NONFINITE_FORCE);
   }
   if (!tvalid) return;
@@ -151,10 +155,11 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   P.icount[s] = cnt;
   const uint32_t o = s - P.own_lo;
   if (P.mode == 0) {
-    if (P.acc_st) {
-      P.acc_st[3 * (size_t)o + 0] = gx;
-      P.acc_st[3 * (size_t)o + 1] = gy;
-      P.acc_st[3 * (size_t)o + 2] = gz;
+    if (P.acc_out) {
+      const size_t k = P.user_order ? (size_t)P.uid[s] : (size_t)o;
+      P.acc_out[3 * k + 0] = gx;
+      P.acc_out[3 * k + 1] = gy;
+      P.acc_out[3 * k + 2] = gz;
     }
   } else {
     float4 v = P.vel4[o];
@@ -180,7 +185,8 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.icount = W.icount;
   P.pos4 = W.pos4;
   P.vel4 = W.vel4;
-  P.acc_st = a.acc_out;
+  P.acc_out = a.acc_out;
+  P.user_order = a.user_order;
   P.n_targets = a.n_targets;
   P.use_targets = a.use_targets;
   P.mode = a.mode;
