@@ -162,7 +162,7 @@ typedef struct {
     int64_t own_begin, own_end; /* this rank's range of storage indices          */
     int64_t steps;          /* steps taken since create / set_state              */
     int64_t opens;          /* last walk: MAC tests that opened a node             */
-    int64_t interactions_cum; /* all walks since create / set_state              */
+    int64_t interactions_cum; /* all walks since bh_create                        */
     int64_t opens_cum;
 } bh_stats;
 bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);

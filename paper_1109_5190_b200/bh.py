@@ -142,7 +142,9 @@ class BarnesHut:
         self.n = n
         self.device = device
         torch.cuda.set_device(device)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        # a dedicated (non-default) stream: all of the ctx's work is enqueued on it and
+        # callers time it with events recorded on self.stream
+        self.stream = stream if stream is not None else torch.cuda.Stream(device)
         p = BhParams(n=n, theta=float(theta), eps=float(eps), G=float(G), dt=float(dt), device=device, rank=rank,
                      world=world, stream=C.c_void_p(self.stream.cuda_stream), nccl_comm=nccl_comm,
                      workspace=None, workspace_bytes=0, node_capacity=int(node_capacity),
@@ -157,6 +159,7 @@ class BarnesHut:
         self.params = p
         h = C.c_void_p()
         if on_dev:
+            self.stream.wait_stream(torch.cuda.current_stream(device))  # inputs made on the caller's stream
             m_, p_, v_ = (mass.contiguous().float(), pos.contiguous().float(),
                           None if vel is None else vel.contiguous().float())
             rc = self.L.bh_create(C.byref(h), C.byref(p), _ptr(m_), _ptr(p_), _ptr(v_), BH_DEVICE)
@@ -190,6 +193,7 @@ class BarnesHut:
         if isinstance(pos, torch.Tensor) and pos.is_cuda:
             self._keep = (mass.contiguous().float(), pos.contiguous().float(),
                           None if vel is None else vel.contiguous().float())
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
             self._chk(self.L.bh_set_state(self.h, *map(_ptr, self._keep), BH_DEVICE))
         else:
             n = self.n
@@ -205,7 +209,10 @@ class BarnesHut:
         """Accelerations [n,3] (user order).  `out`: a CUDA tensor to fill
         asynchronously; default returns a host numpy array."""
         if out is not None:
+            cur = self.torch.cuda.current_stream(self.device)
+            self.stream.wait_stream(cur)
             self._chk(self.L.bh_compute_forces(self.h, _ptr(out), BH_DEVICE))
+            cur.wait_stream(self.stream)  # the caller's stream sees the result
             return out
         a = np.zeros((self.n, 3), np.float32)
         self._chk(self.L.bh_compute_forces(self.h, _ptr(a), BH_HOST))
@@ -219,7 +226,10 @@ class BarnesHut:
 
     def get_state(self, pos_out=None, vel_out=None):
         if pos_out is not None or vel_out is not None:
+            cur = self.torch.cuda.current_stream(self.device)
+            self.stream.wait_stream(cur)
             self._chk(self.L.bh_get_state(self.h, _ptr(pos_out), _ptr(vel_out), BH_DEVICE))
+            cur.wait_stream(self.stream)
             return pos_out, vel_out
         pos = np.zeros((self.n, 3), np.float32)
         vel = np.zeros((self.n, 3), np.float32)

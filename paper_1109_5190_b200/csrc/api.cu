@@ -550,7 +550,6 @@ bh_status bh_set_state(bh_ctx *ctx, const float *mass, const float *pos, const f
                                                         ctx->own_lo, ctx->own_hi);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(&ctx->W.status->err, 0, sizeof(uint32_t), ctx->stream));
-  CK(cudaMemsetAsync(&ctx->W.status->interactions_cum, 0, 2 * sizeof(unsigned long long), ctx->stream));
   ctx->steps = 0;
   ctx->tree_valid = false;
   return BH_OK;
