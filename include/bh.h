@@ -164,6 +164,7 @@ typedef struct {
     int64_t opens;          /* last walk: MAC tests that opened a node             */
     int64_t interactions_cum; /* all walks since bh_create                        */
     int64_t opens_cum;
+    int64_t lane_iters;     /* last walk: traversal-loop iterations x lanes (SIMD slots) */
 } bh_stats;
 bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);
 

@@ -57,6 +57,7 @@ class BhStats(C.Structure):
         ("opens", C.c_int64),
         ("interactions_cum", C.c_int64),
         ("opens_cum", C.c_int64),
+        ("lane_iters", C.c_int64),
     ]
 
 

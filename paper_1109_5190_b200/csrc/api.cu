@@ -371,7 +371,7 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.own_lo = (uint32_t)ctx->own_lo;
   a.acc_out = mode == 0 ? acc_out : nullptr;
   a.user_order = user_order ? 1 : 0;
-  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 3 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 4 * sizeof(unsigned long long), s));
   if (ctx->p.world > 1) {
     CK(launch_own_targets(ctx->W, n, ctx->sort_buf, (uint32_t)ctx->own_lo, (uint32_t)ctx->own_hi, s));
     a.use_targets = 1;
@@ -803,6 +803,7 @@ bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out) {
   out->interactions = (int64_t)ctx->hstatus->interactions;
   out->mac_fallbacks = (int64_t)ctx->hstatus->fallbacks;
   out->opens = (int64_t)ctx->hstatus->opens;
+  out->lane_iters = (int64_t)ctx->hstatus->iters;
   out->interactions_cum = (int64_t)ctx->hstatus->interactions_cum;
   out->opens_cum = (int64_t)ctx->hstatus->opens_cum;
   out->own_begin = ctx->own_lo;

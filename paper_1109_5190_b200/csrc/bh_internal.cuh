@@ -52,7 +52,7 @@ struct DevStatus {
   unsigned long long interactions;   // last walk
   unsigned long long fallbacks;      // last walk: fp64 MAC re-evaluations
   unsigned long long opens;          // last walk: MAC tests that opened a node (incl. self leaf)
-  unsigned long long pad64;
+  unsigned long long iters;          // last walk: group-loop iterations summed over lanes
   unsigned long long interactions_cum;  // since create / set_state
   unsigned long long opens_cum;
   float lo[3];

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   }
   const bool gvalid = (__ballot_sync(full, tvalid) & gmask) != 0u;
   uint32_t c = gvalid ? 0u : Wn;
-  uint32_t resume = 0, cnt = 0, fb = 0, nop = 0;
+  uint32_t resume = 0, cnt = 0, fb = 0, nop = 0, nit = 0;
   int bad = 0;
   float ax = 0.f, ay = 0.f, az = 0.f;
   double dax = 0.0, day = 0.0, daz = 0.0;
@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
     } else {
       if (!__any_sync(full, live)) break;
     }
+    nit += live;
     const uint32_t cc = live ? c : 0u;
     const float4 cm = __ldg(&P.rec_cm[cc]);
     const uint4 au = __ldg(&P.rec_aux[cc]);
@@ -137,17 +138,19 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   }
   dax += ax; day += ay; daz += az;
   // warp reductions of the counters
-  unsigned long long wc = cnt, wf = fb, wo = nop;
+  unsigned long long wc = cnt, wf = fb, wo = nop, wi = nit;
   for (int o = 16; o; o >>= 1) {
     wc += __shfl_xor_sync(full, wc, o);
     wf += __shfl_xor_sync(full, wf, o);
     wo += __shfl_xor_sync(full, wo, o);
+    wi += __shfl_xor_sync(full, wi, o);
   }
   const int wbad = __any_sync(full, bad);
   if (lane == 0) {
     if (wc) { atomicAdd(&P.st->interactions, wc); atomicAdd(&P.st->interactions_cum, wc); }
     if (wf) atomicAdd(&P.st->fallbacks, wf);
     if (wo) { atomicAdd(&P.st->opens, wo); atomicAdd(&P.st->opens_cum, wo); }
+    if (wi) atomicAdd(&P.st->iters, wi);
     if (wbad) atomicOr(&P.st->err, ERR_NONFINITE_FORCE);
   }
   if (!tvalid) return;

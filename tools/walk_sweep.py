@@ -41,7 +41,7 @@ def main():
         fl = 18 * st["interactions"] + 8 * st["opens"]
         print(json.dumps({"config": a.config, "n": int(m.shape[0]), "group": g, "walk_ms": ms,
                           "interactions": st["interactions"], "opens": st["opens"],
-                          "fallbacks": st["mac_fallbacks"], "inter_per_s": st["interactions"] / ms * 1e3,
+                          "fallbacks": st["mac_fallbacks"], "simd_eff": (st["interactions"] + st["opens"]) / max(1, st["lane_iters"]), "inter_per_s": st["interactions"] / ms * 1e3,
                           "tflops": fl / ms / 1e9}), flush=True)
         bh.close()
 
