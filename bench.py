@@ -248,7 +248,14 @@ def ours_arm(args):
     bh.set_profiling(False)
     ms = allreduce(ms_local, dist.ReduceOp.MAX if world > 1 else None)
     inter_local = st1["interactions_cum"] - st0["interactions_cum"]
-    opens_local = st1["opens_cum"] - st0["opens_cum"]
+    # opened-node count (for the flop model) from one untimed stats walk on the
+    # final state: the timed walks run without the stats counters
+    bh.set_walk_stats(True)
+    bh.build_tree()
+    bh._chk(bh.L.bh_compute_forces(bh.h, None, bhmod.BH_DEVICE))
+    sts = bh.get_stats()
+    bh.set_walk_stats(False)
+    opens_local = inter_local * sts["opens"] / max(1, sts["interactions"])
     inter = allreduce(float(inter_local), dist.ReduceOp.SUM if world > 1 else None)
     opens = allreduce(float(opens_local), dist.ReduceOp.SUM if world > 1 else None)
     secs = ms / 1e3
@@ -320,7 +327,9 @@ def ours_arm(args):
                          "peak_source": f"derived: 2 flop x 128 FP32 lanes x {sms} SMs x {sm_max:.0f} MHz "
                                         "(sm_max_mhz of MEASURED_PEAKS.json; B200_PROFILING.md)",
                          "flops_per_launch": flops_walk_launch, "launch_ms": walk_ms,
-                         "flop_model": "18 per interaction + 8 per opened node"},
+                         "flop_model": "18 per interaction + 8 per opened node (opens/interaction ratio from an "
+                                       "untimed stats walk on the final state)",
+                         "simd_efficiency": (sts["interactions"] + sts["opens"]) / max(1, sts["lane_iters"])},
             "hbm_stages": {"sort_GBps": sort_gbs, "sort_bytes_model": "8 passes x 24 B/particle",
                            "hbm_peak_GBps": peaks.get("hbm_gbs")},
             "phase_ms_per_step": phase_ms,

@@ -165,6 +165,7 @@ typedef struct {
     int64_t interactions_cum; /* all walks since bh_create                        */
     int64_t opens_cum;
     int64_t lane_iters;     /* last walk: traversal-loop iterations x lanes (SIMD slots) */
+    int64_t redo_targets;   /* last walk: targets re-walked with the exact fp64 MAC        */
 } bh_stats;
 bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);
 
@@ -173,6 +174,10 @@ bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);
  * 3 moments, 4 walk(+integrate), 5 exchange.  ms[6], launches[6]. */
 bh_status bh_set_profiling(bh_ctx *ctx, int enable);
 bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *calls);
+
+/* Walk statistics (opens, lane_iters of bh_get_stats) cost a few instructions
+ * per visited node; they are off by default (interactions are always counted). */
+bh_status bh_set_walk_stats(bh_ctx *ctx, int enable);
 
 const char *bh_last_error(const bh_ctx *ctx);
 const char *bh_status_string(int status);

@@ -58,6 +58,7 @@ class BhStats(C.Structure):
         ("interactions_cum", C.c_int64),
         ("opens_cum", C.c_int64),
         ("lane_iters", C.c_int64),
+        ("redo_targets", C.c_int64),
     ]
 
 
@@ -99,6 +100,7 @@ def load_library(path: str = LIB_PATH):
             "bh_get_interactions": (i32, [vp, vp, vp]),
             "bh_get_stats": (i32, [vp, C.POINTER(BhStats)]),
             "bh_set_profiling": (i32, [vp, i32]),
+            "bh_set_walk_stats": (i32, [vp, i32]),
             "bh_get_profile": (i32, [vp, vp, vp, vp]),
             "bh_last_error": (C.c_char_p, [vp]),
             "bh_status_string": (C.c_char_p, [i32]),
@@ -283,6 +285,9 @@ class BarnesHut:
         s = BhStats()
         self._chk(self.L.bh_get_stats(self.h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in BhStats._fields_}
+
+    def set_walk_stats(self, on=True):
+        self._chk(self.L.bh_set_walk_stats(self.h, 1 if on else 0))
 
     def set_profiling(self, on=True):
         self._chk(self.L.bh_set_profiling(self.h, 1 if on else 0))

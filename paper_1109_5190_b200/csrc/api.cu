@@ -36,6 +36,7 @@ struct bh_ctx {
   int64_t steps;
   bool tree_valid;
   bool walked;
+  int walk_stats;
   int sort_buf;
   DevStatus *hstatus;  // pinned
   cudaEvent_t status_ev;
@@ -86,7 +87,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
   L.n_own_max = (n + world - 1) / world + 1;
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-  size_t sz[21] = {
+  size_t sz[22] = {
       sizeof(DevStatus),                       // 0 status
       (size_t)n * 16,                          // 1 pos4
       (size_t)L.n_own_max * 16,                // 2 vel4
@@ -103,14 +104,15 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
       (size_t)L.scan_tiles * 4,                // 13 scan_tmp
       sizeof(uint32_t) * (SORT_PASSES * SORT_RADIX + 8 + (size_t)SORT_PASSES * L.sort_tiles * SORT_RADIX),  // 14
       sizeof(float) * 8 * BBOX_BLOCKS,         // 15 bbox partials
-      (size_t)L.cap_rec * 16,                  // 16 rec_cm
-      (size_t)L.cap_rec * 16,                  // 17 rec_aux
+      (size_t)L.cap_rec * 32,                  // 16 rec (cm + aux)
+      0,                                       // 17 (unused)
       (size_t)L.cap_rec * 4,                   // 18 rec_first
       (size_t)L.cap_rec * 32,                  // 19 rec_mom
       (size_t)L.cap_int * 4,                   // 20 lvl_list
+      (size_t)n * 4,                           // 21 redo list
   };
   size_t off = 0;
-  for (int i = 0; i < 21; i++) {
+  for (int i = 0; i < 22; i++) {
     L.off[i] = off;
     off += align_up(sz[i]);
   }
@@ -138,11 +140,11 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.sort_tilectr = W.sort_hist + SORT_PASSES * SORT_RADIX;
   W.sort_status = W.sort_tilectr + 8;
   W.bbox_part = (float *)(b + L.off[15]);
-  W.rec_cm = (float4 *)(b + L.off[16]);
-  W.rec_aux = (uint4 *)(b + L.off[17]);
+  W.rec = (Rec *)(b + L.off[16]);
   W.rec_first = (uint32_t *)(b + L.off[18]);
   W.rec_mom = (double4 *)(b + L.off[19]);
   W.lvl_list = (uint32_t *)(b + L.off[20]);
+  W.redo = (uint32_t *)(b + L.off[21]);
 }
 
 // ---------------------------------------------------------------- small kernels
@@ -362,6 +364,7 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.n = n;
   a.buf = ctx->sort_buf;
   a.group = ctx->p.walk_group ? ctx->p.walk_group : 32;
+  a.stats = ctx->walk_stats;
   a.mode = mode;
   a.eps2 = (float)(ctx->p.eps * ctx->p.eps);
   a.G = (float)ctx->p.G;
@@ -371,7 +374,7 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.own_lo = (uint32_t)ctx->own_lo;
   a.acc_out = mode == 0 ? acc_out : nullptr;
   a.user_order = user_order ? 1 : 0;
-  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 4 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 5 * sizeof(unsigned long long), s));
   if (ctx->p.world > 1) {
     CK(launch_own_targets(ctx->W, n, ctx->sort_buf, (uint32_t)ctx->own_lo, (uint32_t)ctx->own_hi, s));
     a.use_targets = 1;
@@ -412,7 +415,7 @@ static bh_status exchange(bh_ctx *ctx) {
 }
 
 // copy caller inputs (user order) into device scratch: pos -> accu, mass -> targets,
-// vel -> rec_aux region; returns device pointers
+// vel -> the record region; returns device pointers
 static bh_status stage_inputs(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int where,
                               const float **dm, const float **dp, const float **dv) {
   const int64_t n = ctx->p.n;
@@ -422,7 +425,7 @@ static bh_status stage_inputs(bh_ctx *ctx, const float *mass, const float *pos, 
   }
   float *sp = ctx->W.accu;
   float *sm = (float *)ctx->W.targets;
-  float *sv = (float *)ctx->W.rec_aux;
+  float *sv = (float *)ctx->W.rec;
   CK(cudaMemcpyAsync(sp, pos, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(sm, mass, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (vel) CK(cudaMemcpyAsync(sv, vel, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
@@ -484,6 +487,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->steps = 0;
   ctx->tree_valid = false;
   ctx->walked = false;
+  ctx->walk_stats = 0;
   ctx->sort_buf = 0;
   ctx->status_pending = false;
   bh_status st = BH_OK;
@@ -515,14 +519,15 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
     if (launch_bbox(ctx->W, n, s) != cudaSuccess || launch_keys(ctx->W, n, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "keys launch failed"); break; }
     int buf = 0;
     if (launch_sort(ctx->W, n, s, &buf) != cudaSuccess || launch_tie_fixup(ctx->W, n, buf, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "sort launch failed"); break; }
-    // relabel: gather user-order pos4 into rec_cm, copy back; uid[p] = user index
-    k_relabel<<<blocks_for(n), 256, 0, s>>>(ctx->W.rec_cm, ctx->W.pos4, ctx->W.vals[buf], ctx->W.uid, n);
-    if (cudaMemcpyAsync(ctx->W.pos4, ctx->W.rec_cm, (size_t)n * 16, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "copy failed"); break; }
+    // relabel: gather user-order pos4 into the record scratch, copy back; uid[p] = user index
+    float4 *scratch = (float4 *)ctx->W.rec;
+    k_relabel<<<blocks_for(n), 256, 0, s>>>(scratch, ctx->W.pos4, ctx->W.vals[buf], ctx->W.uid, n);
+    if (cudaMemcpyAsync(ctx->W.pos4, scratch, (size_t)n * 16, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "copy failed"); break; }
     int64_t own_n = ctx->own_hi - ctx->own_lo;
     if (dv) {
-      // vel4[s - lo] = vtmp[uid[s]] for own s: reuse relabel into rec_cm then copy the own slice
-      k_relabel<<<blocks_for(n), 256, 0, s>>>(ctx->W.rec_cm, vtmp, ctx->W.vals[buf], ctx->W.uid, n);
-      if (cudaMemcpyAsync(ctx->W.vel4, ctx->W.rec_cm + ctx->own_lo, (size_t)own_n * 16, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "copy failed"); break; }
+      // vel4[s - lo] = vtmp[uid[s]] for own s: relabel into the scratch then copy the own slice
+      k_relabel<<<blocks_for(n), 256, 0, s>>>(scratch, vtmp, ctx->W.vals[buf], ctx->W.uid, n);
+      if (cudaMemcpyAsync(ctx->W.vel4, scratch + ctx->own_lo, (size_t)own_n * 16, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "copy failed"); break; }
     } else {
       if (cudaMemsetAsync(ctx->W.vel4, 0, (size_t)own_n * 16, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
     }
@@ -718,21 +723,18 @@ static bh_status export_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint3
   if (st) return st;
   const int64_t n = ctx->p.n;
   const uint32_t nrec = ctx->hstatus->n_records;
-  std::vector<uint4> aux(nrec);
+  std::vector<Rec> rec(nrec);
   std::vector<uint32_t> fst(nrec);
-  std::vector<float4> cm;
   std::vector<double4> mom;
-  CK(cudaMemcpy(aux.data(), ctx->W.rec_aux, (size_t)nrec * 16, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(rec.data(), ctx->W.rec, (size_t)nrec * sizeof(Rec), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(fst.data(), ctx->W.rec_first, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
   if (M || MX) {
-    cm.resize(nrec);
     mom.resize(nrec);
-    CK(cudaMemcpy(cm.data(), ctx->W.rec_cm, (size_t)nrec * 16, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(mom.data(), ctx->W.rec_mom, (size_t)nrec * 32, cudaMemcpyDeviceToHost));
   }
   int64_t k = 0;
   for (uint32_t c = 0; c < nrec; c++) {
-    const uint4 a = aux[c];
+    const uint4 a = rec[c].aux;
     if (a.w & META_MEMBER) continue;
     if (k < cap) {
       const bool leaf = (a.w & META_LEAF) != 0;
@@ -742,8 +744,9 @@ static bh_status export_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint3
       if (M || MX) {
         double m, x, y, z;
         if (leaf) {
-          m = (double)cm[c].w;
-          x = m * (double)cm[c].x; y = m * (double)cm[c].y; z = m * (double)cm[c].z;
+          const float4 q = rec[c].cm;
+          m = (double)q.w;
+          x = m * (double)q.x; y = m * (double)q.y; z = m * (double)q.z;
         } else {
           m = mom[c].x; x = mom[c].y; y = mom[c].z; z = mom[c].w;
         }
@@ -804,6 +807,7 @@ bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out) {
   out->mac_fallbacks = (int64_t)ctx->hstatus->fallbacks;
   out->opens = (int64_t)ctx->hstatus->opens;
   out->lane_iters = (int64_t)ctx->hstatus->iters;
+  out->redo_targets = (int64_t)ctx->hstatus->n_redo;
   out->interactions_cum = (int64_t)ctx->hstatus->interactions_cum;
   out->opens_cum = (int64_t)ctx->hstatus->opens_cum;
   out->own_begin = ctx->own_lo;
@@ -835,6 +839,12 @@ bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *ca
   }
   if (calls) *calls = ctx->prof_calls;
   return st;
+}
+
+bh_status bh_set_walk_stats(bh_ctx *ctx, int enable) {
+  if (!ctx) return BH_ERR_ARG;
+  ctx->walk_stats = enable ? 1 : 0;
+  return BH_OK;
 }
 
 bh_status bh_nccl_unique_id(void *id128) {

@@ -12,8 +12,10 @@
 //   walk records    : DFS pre-order array of tree nodes where every particle
 //                     has exactly one record (a single-particle leaf, or a
 //                     "member" record right after its level-21 bucket):
-//                       rec_cm[c]  float4 (com32.xyz, M32)       16 B
-//                       rec_aux[c] uint4  (T_acc, T_rej, skip, meta) 16 B
+//                       rec[c].cm  float4 (com32.xyz, M32)       16 B
+//                       rec[c].aux uint4  (T_acc, T_rej, skip, meta) 16 B
+//                       (one 32-byte sector per record: a lane's visit
+//                       touches one sector)
 //                       rec_first[c] u32 first sorted particle  (export)
 //                       rec_mom[c] double4 (M, MX, MY, MZ) fp64 (internal)
 //                     skip(c) = index of the first record after c's subtree,
@@ -29,7 +31,7 @@
 
 namespace bh {
 
-// meta bits of rec_aux[c].w
+// meta bits of rec[c].aux.w
 enum : uint32_t {
   META_LEVEL_MASK = 0x1f,  // level 0..21; 22 for bucket members
   META_LEAF = 1u << 5,     // single-particle leaf or bucket member (has no children)
@@ -49,10 +51,12 @@ struct DevStatus {
   uint32_t n_records;   // total walk records (nstart[n])
   uint32_t n_internal;
   uint32_t bbox_ticket; // last-block ticket of the bbox reduction
+  // per-walk counters (zeroed before every walk; kept contiguous)
   unsigned long long interactions;   // last walk
   unsigned long long fallbacks;      // last walk: fp64 MAC re-evaluations
   unsigned long long opens;          // last walk: MAC tests that opened a node (incl. self leaf)
   unsigned long long iters;          // last walk: group-loop iterations summed over lanes
+  unsigned long long n_redo;         // last walk: targets re-walked with the exact fp64 MAC
   unsigned long long interactions_cum;  // since create / set_state
   unsigned long long opens_cum;
   float lo[3];
@@ -62,6 +66,11 @@ struct DevStatus {
   uint32_t lvl_count[24];   // internal nodes per level (0..21)
   uint32_t lvl_offset[24];  // exclusive prefix of lvl_count
   uint32_t lvl_cursor[24];
+};
+
+struct __align__(32) Rec {
+  float4 cm;
+  uint4 aux;
 };
 
 struct Workspace {
@@ -75,13 +84,13 @@ struct Workspace {
   uint32_t *icount;   // interactions per storage id
   float *accu;        // n * 3, user order (BH_HOST force output staging)
   uint32_t *targets;  // own sorted positions (world > 1)
+  uint32_t *redo;     // target slots whose fp32 MAC filter was inconclusive
   uint32_t *scan_tmp; // scan tile partials
   uint32_t *sort_hist;    // 8 x 256
   uint32_t *sort_status;  // 8 passes x tiles x 256
   uint32_t *sort_tilectr; // 8
   float *bbox_part;       // partial min/max per block (8 floats)
-  float4 *rec_cm;
-  uint4 *rec_aux;
+  Rec *rec;
   uint32_t *rec_first;
   double4 *rec_mom;
   uint32_t *lvl_list;
@@ -128,6 +137,7 @@ struct WalkArgs {
   int use_targets;      // 1: targets[] holds sorted positions; 0: target t is sorted position t
   int buf;              // sort buffer holding vals
   int group;            // lanes per shared traversal
+  int stats;            // 1: also count opened nodes and SIMD slots
   int mode;             // 0 = forces to acc_out (user order), 1 = fused leapfrog
   float eps2, G;
   float kick, dt;       // mode 1

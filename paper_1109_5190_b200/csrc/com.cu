@@ -41,7 +41,7 @@ __device__ __forceinline__ float round_down_f(double x) {
 
 __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatus *__restrict__ st,
                                                        const uint32_t *__restrict__ lvl_list,
-                                                       float4 *__restrict__ rec_cm, uint4 *__restrict__ rec_aux,
+                                                       Rec *__restrict__ rec,
                                                        double4 *__restrict__ rec_mom, double theta) {
   if (st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t cnt = st->lvl_count[level];
@@ -49,14 +49,14 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
   const double Ld = (double)st->L;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
     const uint32_t c = lvl_list[off + t];
-    const uint4 aux = rec_aux[c];
+    const uint4 aux = rec[c].aux;
     const uint32_t end = aux.z;
     double M = 0.0, X = 0.0, Y = 0.0, Z = 0.0;
     uint32_t ch = c + 1;
     while (ch < end) {
-      uint4 ca = rec_aux[ch];
+      uint4 ca = rec[ch].aux;
       if (ca.w & META_LEAF) {
-        float4 p = rec_cm[ch];
+        float4 p = rec[ch].cm;
         double m = (double)p.w;
         M = __dadd_rn(M, m);
         X = __dadd_rn(X, __dmul_rn(m, (double)p.x));
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
     rec_mom[c] = make_double4(M, X, Y, Z);
     const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
     const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
-    rec_cm[c] = make_float4(fx, fy, fz, __double2float_rn(M));
+    rec[c].cm = make_float4(fx, fy, fz, __double2float_rn(M));
     float tacc, trej;
     if (!(theta > 0.0)) {
       tacc = INFINITY;
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
       const double B = (r * (1.0 - delta) - b) / (1.0 + a);
       trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 1e-15)) : -INFINITY;
     }
-    rec_aux[c] = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), aux.z, aux.w);
+    rec[c].aux = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), aux.z, aux.w);
   }
 }
 
@@ -105,7 +105,7 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, int64_t cap_rec, int64
   int grid = (int)(need < lim ? need : lim);
   if (grid < 1) grid = 1;
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
-    k_moments_level<<<grid, 256, 0, s>>>(l, W.status, W.lvl_list, W.rec_cm, W.rec_aux, W.rec_mom, theta);
+    k_moments_level<<<grid, 256, 0, s>>>(l, W.status, W.lvl_list, W.rec, W.rec_mom, theta);
     if (launches) (*launches)++;
   }
   return cudaGetLastError();

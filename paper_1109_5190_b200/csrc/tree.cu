@@ -92,8 +92,8 @@ __device__ __forceinline__ int64_t run_end(const unsigned long long *__restrict_
 __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restrict__ keys,
                                               const uint32_t *__restrict__ vals, const uint8_t *__restrict__ lcp,
                                               const uint32_t *__restrict__ nstart, const float4 *__restrict__ pos4,
-                                              int64_t n, DevStatus *st, float4 *__restrict__ rec_cm,
-                                              uint4 *__restrict__ rec_aux, uint32_t *__restrict__ rec_first,
+                                              int64_t n, DevStatus *st, Rec *__restrict__ rec,
+                                              uint32_t *__restrict__ rec_first,
                                               uint32_t *__restrict__ lvl_list) {
   __shared__ uint32_t cnt[24], slot[24], gb[24];
   if (st->err & ERR_NODE_OVERFLOW) return;  // uniform: nothing safe to write
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
     uint32_t skip = nstart[e + 1];
     rec_first[c] = (uint32_t)p;
     uint32_t meta = (uint32_t)l | (l == BH_MAXLEVEL ? META_BUCKET : 0u);
-    rec_aux[c] = make_uint4(0u, 0u, skip, meta);
+    rec[c].aux = make_uint4(0u, 0u, skip, meta);
     uint32_t s = atomicAdd(&slot[l], 1u);
     lvl_list[gb[l] + s] = c;
   }
@@ -129,9 +129,9 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
   uint32_t meta = top + 1 <= BH_MAXLEVEL ? ((uint32_t)(top + 1) | META_LEAF)
                                          : ((uint32_t)(BH_MAXLEVEL + 1) | META_LEAF | META_MEMBER);
   rec_first[c] = (uint32_t)p;
-  rec_cm[c] = pos4[vals[p]];
+  rec[c].cm = pos4[vals[p]];
   // T_acc = -inf: a particle record is always "accepted" unless it is the target
-  rec_aux[c] = make_uint4(__float_as_uint(-INFINITY), __float_as_uint(-INFINITY), c + 1u, meta);
+  rec[c].aux = make_uint4(__float_as_uint(-INFINITY), __float_as_uint(-INFINITY), c + 1u, meta);
 }
 
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, cudaStream_t s) {
@@ -144,7 +144,7 @@ cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf,
   // cap_int: the level list holds at most cap_rec - n internal nodes
   k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, cap_rec - n, W.status);
   k_emit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.lcp, W.nstart, W.pos4, n,
-                                                     W.status, W.rec_cm, W.rec_aux, W.rec_first, W.lvl_list);
+                                                     W.status, W.rec, W.rec_first, W.lvl_list);
   return cudaGetLastError();
 }
 

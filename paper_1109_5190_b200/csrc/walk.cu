@@ -17,13 +17,17 @@
 // Barnes-Hut frontier, in DFS order -- identical decisions to the oracle's
 // recursive walk -- while the group's record loads are one broadcast address.
 //
-// MAC decisions are exact: the fp32 test uses the per-node thresholds T_acc /
-// T_rej of com.cu; only when d2_32 falls between them is the oracle's fp64
-// formula re-evaluated from the fp64 moments (counted in `fallbacks`).
+// MAC decisions are exact.  The fast kernel decides with the fp32 thresholds
+// T_acc / T_rej of com.cu (d2_32 > T_acc: accept for sure; d2_32 < T_rej: open
+// for sure).  A lane whose d2_32 falls between them (~1e-6 of the tests) drops
+// out of the fast walk and is queued; k_walk_exact then re-walks those targets
+// alone with the oracle's fp64 test on the ambiguous nodes.  The fast loop thus
+// carries no fp64 code and no divergent branch.
 //
 // Interaction (fp32): r2 = d2 + eps^2, f = M rsqrt(r2)^3, a += f (dx, dy, dz):
-// 18 flops + 1 MUFU.RSQ.  Partial sums are folded into fp64 every 64 interactions of
-// the lane, so the result does not depend on the group size or the rank count.
+// 18 flops + 1 MUFU.RSQ.  Partial sums are folded into fp64 at every 64th
+// interaction of the lane (a per-lane rule: the result does not depend on the
+// group size or the rank count).
 //
 // K7 (mode 1): v += a * kick (kick = dt/2 on the first step, dt after; reading
 // L8), x += v dt, written in place to pos4 / vel4 of the particle's storage slot
@@ -35,8 +39,7 @@
 namespace bh {
 
 struct WalkParams {
-  const float4 *__restrict__ rec_cm;
-  const uint4 *__restrict__ rec_aux;
+  const Rec *__restrict__ rec;
   const double4 *__restrict__ rec_mom;
   const uint32_t *__restrict__ nstart;
   const uint32_t *__restrict__ vals;
@@ -44,6 +47,7 @@ struct WalkParams {
   const uint32_t *__restrict__ uid;
   DevStatus *st;
   uint32_t *icount;
+  uint32_t *redo;
   float4 *pos4;
   float4 *vel4;
   float *acc_out;  // mode 0: acc_out[3 uid[s]] (user_order) or acc_out[3 (s - own_lo)]
@@ -55,6 +59,12 @@ struct WalkParams {
   double theta2;
   uint32_t own_lo;
 };
+
+__device__ __forceinline__ float rsqrt_fast(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __noinline__ bool exact_accept(const double4 *__restrict__ rec_mom, uint32_t c, uint32_t level, float x,
                                           float y, float z, double L, double theta2) {
@@ -70,96 +80,30 @@ __device__ __noinline__ bool exact_accept(const double4 *__restrict__ rec_mom, u
   return s2 < __dmul_rn(theta2, d2);
 }
 
-template <int G>
-__global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
-  const uint32_t full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const uint32_t gmask = G == 32 ? full : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  if (P.st->err & ERR_NODE_OVERFLOW) return;
-  const uint32_t Wn = P.st->n_records;
-  const double Ld = (double)P.st->L;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool tvalid = t < P.n_targets;
-  uint32_t p = 0, Li = 0, s = 0;
-  float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (tvalid) {
-    p = P.use_targets ? P.targets[t] : (uint32_t)t;
-    Li = P.nstart[p + 1] - 1u;
-    me = P.rec_cm[Li];
-    s = P.vals[p];
-  }
-  const bool gvalid = (__ballot_sync(full, tvalid) & gmask) != 0u;
-  uint32_t c = gvalid ? 0u : Wn;
-  uint32_t resume = 0, cnt = 0, fb = 0, nop = 0, nit = 0;
-  int bad = 0;
-  float ax = 0.f, ay = 0.f, az = 0.f;
-  double dax = 0.0, day = 0.0, daz = 0.0;
-  for (;;) {
-    const bool live = c < Wn;
-    if (G == 32) {
-      if (!live) break;
-    } else {
-      if (!__any_sync(full, live)) break;
-    }
-    nit += live;
-    const uint32_t cc = live ? c : 0u;
-    const float4 cm = __ldg(&P.rec_cm[cc]);
-    const uint4 au = __ldg(&P.rec_aux[cc]);
-    const uint32_t skip = au.z;
-    const float dx = cm.x - me.x, dy = cm.y - me.y, dz = cm.z - me.z;
-    const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    const bool act = live && tvalid && c >= resume;
-    const bool cont = (c <= Li) && (Li < skip);
-    bool acc = act && !cont && d2 > __uint_as_float(au.x);
-    const bool amb = act && !cont && !acc && !(d2 < __uint_as_float(au.y));
-    if (amb) {
-      acc = exact_accept(P.rec_mom, cc, au.w & META_LEVEL_MASK, me.x, me.y, me.z, Ld, P.theta2);
-      fb++;
-    }
-    if (acc) {
-      const float r2 = d2 + P.eps2;
-      bad |= (r2 == 0.0f);
-      const float inv = rsqrtf(r2);
-      const float f = cm.w * (inv * inv) * inv;
-      ax = fmaf(f, dx, ax);
-      ay = fmaf(f, dy, ay);
-      az = fmaf(f, dz, az);
-      cnt++;
-      resume = skip;
-      if ((cnt & 63u) == 0u) {  // fold per lane: results independent of the group size
-        dax += ax; day += ay; daz += az;
-        ax = ay = az = 0.f;
-      }
-    }
-    const bool opn = act && !acc;
-    nop += opn;
-    const uint32_t ob = __ballot_sync(full, opn);
-    if (live) c = (ob & gmask) ? c + 1u : skip;
-  }
-  dax += ax; day += ay; daz += az;
-  // warp reductions of the counters
-  unsigned long long wc = cnt, wf = fb, wo = nop, wi = nit;
-  for (int o = 16; o; o >>= 1) {
-    wc += __shfl_xor_sync(full, wc, o);
-    wf += __shfl_xor_sync(full, wf, o);
-    wo += __shfl_xor_sync(full, wo, o);
-    wi += __shfl_xor_sync(full, wi, o);
-  }
-  const int wbad = __any_sync(full, bad);
-  if (lane == 0) {
-    if (wc) { atomicAdd(&P.st->interactions, wc); atomicAdd(&P.st->interactions_cum, wc); }
-    if (wf) atomicAdd(&P.st->fallbacks, wf);
-    if (wo) { atomicAdd(&P.st->opens, wo); atomicAdd(&P.st->opens_cum, wo); }
-    if (wi) atomicAdd(&P.st->iters, wi);
-    if (wbad) atomicOr(&P.st->err, ERR_NONFINITE_FORCE);
-  }
-  if (!tvalid) return;
+struct Target {
+  uint32_t p, Li, s;
+  float4 me;
+};
+
+__device__ __forceinline__ Target load_target(const WalkParams &P, int64_t t) {
+  Target T;
+  T.p = P.use_targets ? P.targets[t] : (uint32_t)t;
+  T.Li = P.nstart[T.p + 1] - 1u;  // the particle's own record
+  T.me = P.rec[T.Li].cm;
+  T.s = P.vals[T.p];
+  return T;
+}
+
+// outputs of one target: forces (mode 0) or the fused leapfrog (mode 1)
+__device__ __forceinline__ void finish(const WalkParams &P, const Target &T, double dax, double day, double daz,
+                                       uint32_t cnt) {
+  if (!(isfinite(dax) && isfinite(day) && isfinite(daz))) atomicOr(&P.st->err, ERR_NONFINITE_FORCE);
   const float gx = P.G * (float)dax, gy = P.G * (float)day, gz = P.G * (float)daz;
-  P.icount[s] = cnt;
-  const uint32_t o = s - P.own_lo;
+  P.icount[T.s] = cnt;
+  const uint32_t o = T.s - P.own_lo;
   if (P.mode == 0) {
     if (P.acc_out) {
-      const size_t k = P.user_order ? (size_t)P.uid[s] : (size_t)o;
+      const size_t k = P.user_order ? (size_t)P.uid[T.s] : (size_t)o;
       P.acc_out[3 * k + 0] = gx;
       P.acc_out[3 * k + 1] = gy;
       P.acc_out[3 * k + 2] = gz;
@@ -170,15 +114,161 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
     v.y = fmaf(gy, P.kick, v.y);
     v.z = fmaf(gz, P.kick, v.z);
     P.vel4[o] = v;
-    P.pos4[s] = make_float4(fmaf(v.x, P.dt, me.x), fmaf(v.y, P.dt, me.y), fmaf(v.z, P.dt, me.z), me.w);
+    P.pos4[T.s] = make_float4(fmaf(v.x, P.dt, T.me.x), fmaf(v.y, P.dt, T.me.y), fmaf(v.z, P.dt, T.me.z), T.me.w);
+  }
+}
+
+template <int G, bool STATS>
+__global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
+  const uint32_t full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gmask = G == 32 ? full : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  if (P.st->err & ERR_NODE_OVERFLOW) return;
+  const uint32_t Wn = P.st->n_records;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool tvalid = t < P.n_targets;
+  Target T;
+  if (tvalid) T = load_target(P, t);
+  else { T.p = 0; T.Li = 0; T.s = 0; T.me = make_float4(0.f, 0.f, 0.f, 0.f); }
+  const uint32_t Li = T.Li;
+  const float mx = T.me.x, my = T.me.y, mz = T.me.z;
+  const bool gvalid = (__ballot_sync(full, tvalid) & gmask) != 0u;
+  const float eps2 = P.eps2;
+  const Rec *__restrict__ rec = P.rec;
+  uint32_t c = gvalid ? 0u : Wn;
+  // a lane is active at record c iff c >= resume; an invalid (or dropped-out)
+  // lane has resume past every record
+  uint32_t resume = tvalid ? 0u : 0xffffffffu;
+  uint32_t cnt = 0, nop = 0, nit = 0;
+  float ax = 0.f, ay = 0.f, az = 0.f;
+  double dax = 0.0, day = 0.0, daz = 0.0;
+  bool live = c < Wn;
+  // outer loop: the fp64 fold runs on a uniform exit of the inner loop
+  while (G == 32 ? live : __any_sync(full, live)) {
+    bool fold;
+    for (;;) {
+      if (STATS) nit++;
+      const uint32_t cc = (G == 32) ? c : (live ? c : 0u);
+      const float4 cm = __ldg(&rec[cc].cm);
+      const uint4 au = __ldg(&rec[cc].aux);
+      const uint32_t skip = au.z;
+      const float dx = cm.x - mx, dy = cm.y - my, dz = cm.z - mz;
+      const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      // act: past the subtree of the last accepted node; cont: c <= Li < skip
+      const bool act = (G == 32 ? true : live) & (cc >= resume);
+      const bool ok = act & !((cc <= Li) & (skip > Li));
+      const bool acc = ok & (d2 > __uint_as_float(au.x));
+      const bool amb = ok & !acc & (d2 >= __uint_as_float(au.y));
+      const bool opn = act & !acc & !amb;
+      if (STATS) nop += opn;
+      // interaction, branch-free: f = 0 for lanes that do not accept c
+      const float inv = rsqrt_fast(d2 + eps2);
+      float f = cm.w * (inv * inv) * inv;
+      f = acc ? f : 0.0f;
+      ax = fmaf(f, dx, ax);
+      ay = fmaf(f, dy, ay);
+      az = fmaf(f, dz, az);
+      cnt += acc ? 1u : 0u;
+      resume = acc ? skip : (amb ? 0xffffffffu : resume);
+      uint32_t nxt;
+      if (G == 32) {
+        nxt = __any_sync(full, opn) ? cc + 1u : skip;
+        c = nxt;
+      } else {
+        nxt = (__ballot_sync(full, opn) & gmask) ? cc + 1u : skip;
+        c = live ? nxt : c;
+      }
+      live = c < Wn;
+      fold = acc & ((cnt & 63u) == 0u);
+      if (__any_sync(full, fold)) break;
+      if (G == 32 ? !live : !__any_sync(full, live)) break;
+    }
+    if (fold) {
+      dax += ax; day += ay; daz += az;
+      ax = ay = az = 0.f;
+    }
+  }
+  dax += ax; day += ay; daz += az;
+  // warp reductions of the counters
+  // a lane that met an inconclusive MAC test dropped out with resume = ~0u
+  const bool redo = tvalid && resume == 0xffffffffu;
+  unsigned long long wc = redo ? 0u : cnt, wo = nop, wi = nit;
+  for (int o = 16; o; o >>= 1) {
+    wc += __shfl_xor_sync(full, wc, o);
+    if (STATS) {
+      wo += __shfl_xor_sync(full, wo, o);
+      wi += __shfl_xor_sync(full, wi, o);
+    }
+  }
+  if (lane == 0) {
+    if (wc) { atomicAdd(&P.st->interactions, wc); atomicAdd(&P.st->interactions_cum, wc); }
+    if (STATS && wo) { atomicAdd(&P.st->opens, wo); atomicAdd(&P.st->opens_cum, wo); }
+    if (STATS && wi) atomicAdd(&P.st->iters, wi);
+  }
+  if (!tvalid) return;
+  if (redo) {  // re-walked by k_walk_exact
+    unsigned long long k = atomicAdd(&P.st->n_redo, 1ull);
+    P.redo[k] = (uint32_t)t;
+    return;
+  }
+  finish(P, T, dax, day, daz, cnt);
+}
+
+// Exact walk of the queued targets, one lane per target (rare; the fp64 test
+// decides every node the fp32 filter leaves open).
+__global__ void __launch_bounds__(128) k_walk_exact(const WalkParams P) {
+  if (P.st->err & ERR_NODE_OVERFLOW) return;
+  const uint32_t Wn = P.st->n_records;
+  const unsigned long long nredo = P.st->n_redo;
+  const double Ld = (double)P.st->L;
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < nredo;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const Target T = load_target(P, P.redo[k]);
+    uint32_t c = 0, cnt = 0, fb = 0, nop = 0;
+    float ax = 0.f, ay = 0.f, az = 0.f;
+    double dax = 0.0, day = 0.0, daz = 0.0;
+    while (c < Wn) {
+      const float4 cm = P.rec[c].cm;
+      const uint4 au = P.rec[c].aux;
+      const float dx = cm.x - T.me.x, dy = cm.y - T.me.y, dz = cm.z - T.me.z;
+      const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      const bool cont = (c <= T.Li) & (au.z > T.Li);
+      bool acc = !cont & (d2 > __uint_as_float(au.x));
+      if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
+        acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
+        fb++;
+      }
+      if (acc) {
+        const float inv = rsqrt_fast(d2 + P.eps2);
+        const float f = cm.w * (inv * inv) * inv;
+        ax = fmaf(f, dx, ax);
+        ay = fmaf(f, dy, ay);
+        az = fmaf(f, dz, az);
+        cnt++;
+        if ((cnt & 63u) == 0u) {
+          dax += ax; day += ay; daz += az;
+          ax = ay = az = 0.f;
+        }
+        c = au.z;
+      } else {
+        nop++;
+        c = c + 1u;
+      }
+    }
+    dax += ax; day += ay; daz += az;
+    atomicAdd(&P.st->interactions, (unsigned long long)cnt);
+    atomicAdd(&P.st->interactions_cum, (unsigned long long)cnt);
+    atomicAdd(&P.st->fallbacks, (unsigned long long)fb);
+    atomicAdd(&P.st->opens, (unsigned long long)nop);
+    atomicAdd(&P.st->opens_cum, (unsigned long long)nop);
+    finish(P, T, dax, day, daz, cnt);
   }
 }
 
 cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   if (a.n_targets <= 0) return cudaSuccess;
   WalkParams P;
-  P.rec_cm = W.rec_cm;
-  P.rec_aux = W.rec_aux;
+  P.rec = W.rec;
   P.rec_mom = W.rec_mom;
   P.nstart = W.nstart;
   P.vals = W.vals[a.buf];
@@ -186,6 +276,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.uid = W.uid;
   P.st = W.status;
   P.icount = W.icount;
+  P.redo = W.redo;
   P.pos4 = W.pos4;
   P.vel4 = W.vel4;
   P.acc_out = a.acc_out;
@@ -200,14 +291,25 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.theta2 = a.theta2;
   P.own_lo = a.own_lo;
   unsigned grid = (unsigned)((a.n_targets + 255) / 256);
+#define BH_WALK_CASE(g)                                                     \
+  case g:                                                                   \
+    if (a.stats) k_walk<g, true><<<grid, 256, 0, s>>>(P);                   \
+    else k_walk<g, false><<<grid, 256, 0, s>>>(P);                          \
+    break;
   switch (a.group) {
-    case 1: k_walk<1><<<grid, 256, 0, s>>>(P); break;
-    case 2: k_walk<2><<<grid, 256, 0, s>>>(P); break;
-    case 4: k_walk<4><<<grid, 256, 0, s>>>(P); break;
-    case 8: k_walk<8><<<grid, 256, 0, s>>>(P); break;
-    case 16: k_walk<16><<<grid, 256, 0, s>>>(P); break;
-    default: k_walk<32><<<grid, 256, 0, s>>>(P); break;
+    BH_WALK_CASE(1)
+    BH_WALK_CASE(2)
+    BH_WALK_CASE(4)
+    BH_WALK_CASE(8)
+    BH_WALK_CASE(16)
+    default:
+    BH_WALK_CASE(32)
   }
+#undef BH_WALK_CASE
+  // the exact re-walk: a fixed grid, grid-stride over the device-side queue
+  int64_t eg = (a.n_targets + 127) / 128;
+  if (eg > 148 * 4) eg = 148 * 4;
+  k_walk_exact<<<(unsigned)eg, 128, 0, s>>>(P);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,11 @@ def main():
     for g in [int(x) for x in a.groups.split(",")]:
         bh = BarnesHut(m, p, v, walk_group=g, **prm)
         bh.build_tree()
-        bh.compute_forces(None if False else _dev_out(bh))
+        bh.set_walk_stats(True)
+        bh.compute_forces(_dev_out(bh))
+        bh.sync()
+        st_stats = bh.get_stats()
+        bh.set_walk_stats(False)
         bh.sync()
         bh.set_profiling(True)
         for _ in range(a.reps):
@@ -38,10 +42,10 @@ def main():
         prof = bh.get_profile()
         st = bh.get_stats()
         ms = prof["ms"]["walk"] / a.reps
-        fl = 18 * st["interactions"] + 8 * st["opens"]
+        fl = 18 * st["interactions"] + 8 * st_stats["opens"]
         print(json.dumps({"config": a.config, "n": int(m.shape[0]), "group": g, "walk_ms": ms,
-                          "interactions": st["interactions"], "opens": st["opens"],
-                          "fallbacks": st["mac_fallbacks"], "simd_eff": (st["interactions"] + st["opens"]) / max(1, st["lane_iters"]), "inter_per_s": st["interactions"] / ms * 1e3,
+                          "interactions": st["interactions"], "opens": st_stats["opens"], "redo": st["redo_targets"],
+                          "fallbacks": st["mac_fallbacks"], "simd_eff": (st_stats["interactions"] + st_stats["opens"]) / max(1, st_stats["lane_iters"]), "inter_per_s": st["interactions"] / ms * 1e3,
                           "tflops": fl / ms / 1e9}), flush=True)
         bh.close()
 
