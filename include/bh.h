@@ -178,6 +178,10 @@ bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *ca
 /* Walk statistics (opens, lane_iters of bh_get_stats) cost a few instructions
  * per visited node; they are off by default (interactions are always counted). */
 bh_status bh_set_walk_stats(bh_ctx *ctx, int enable);
+/* Per record level 0..22 (22 = bucket members), accumulated over stats-mode
+ * walks since bh_set_walk_stats(ctx, 1): SIMD slots, active lane-visits and
+ * interactions; arrays of 24 (any may be NULL). */
+bh_status bh_get_walk_level_stats(bh_ctx *ctx, int64_t *iters24, int64_t *active24, int64_t *inter24);
 
 const char *bh_last_error(const bh_ctx *ctx);
 const char *bh_status_string(int status);

@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbh.so")
+LIB_PATH = os.environ.get("BH_LIB") or os.path.join(_HERE, "lib", "libbh.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bh.h")
 
 BH_OK, BH_ERR_ARG, BH_ERR_CUDA, BH_ERR_OOM, BH_ERR_STATE, BH_ERR_NONFINITE, BH_ERR_NCCL = 0, -1, -2, -3, -4, -5, -6
@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH):
             "bh_get_stats": (i32, [vp, C.POINTER(BhStats)]),
             "bh_set_profiling": (i32, [vp, i32]),
             "bh_set_walk_stats": (i32, [vp, i32]),
+            "bh_get_walk_level_stats": (i32, [vp, vp, vp, vp]),
             "bh_get_profile": (i32, [vp, vp, vp, vp]),
             "bh_last_error": (C.c_char_p, [vp]),
             "bh_status_string": (C.c_char_p, [i32]),
@@ -288,6 +289,11 @@ class BarnesHut:
 
     def set_walk_stats(self, on=True):
         self._chk(self.L.bh_set_walk_stats(self.h, 1 if on else 0))
+
+    def get_walk_level_stats(self):
+        it, ac, ia = (np.zeros(24, np.int64) for _ in range(3))
+        self._chk(self.L.bh_get_walk_level_stats(self.h, _ptr(it), _ptr(ac), _ptr(ia)))
+        return it, ac, ia
 
     def set_profiling(self, on=True):
         self._chk(self.L.bh_set_profiling(self.h, 1 if on else 0))

@@ -38,9 +38,10 @@ def _newer(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None, objdir_name: str = "build") -> str:
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, objdir_name)
+    lib_out = out or LIB
     os.makedirs(objdir, exist_ok=True)
     inc, lib = nccl_dirs()
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "bh.h")]
@@ -52,18 +53,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if force or _newer(obj, [src] + headers + [__file__]):
             cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                    "-Xptxas", "-v" if verbose else "-O3", "-I", inc, "-I", os.path.join(ROOT, "include"),
-                   "-c", src, "-o", obj]
+                   *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-    if force or _newer(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-L", lib, "-l:libnccl.so.2",
+    if force or _newer(lib_out, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib_out + ".tmp", *objs, "-L", lib, "-l:libnccl.so.2",
                "-Xlinker", f"-rpath,{lib}", "-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib_out + ".tmp", lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

@@ -844,6 +844,25 @@ bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *ca
 bh_status bh_set_walk_stats(bh_ctx *ctx, int enable) {
   if (!ctx) return BH_ERR_ARG;
   ctx->walk_stats = enable ? 1 : 0;
+  if (enable) {
+    bh_status st = set_dev(ctx);
+    if (st) return st;
+    CK(cudaMemsetAsync(ctx->W.status->lvl_iters, 0, 3 * 24 * sizeof(unsigned long long), ctx->stream));
+  }
+  return BH_OK;
+}
+
+bh_status bh_get_walk_level_stats(bh_ctx *ctx, int64_t *iters24, int64_t *active24, int64_t *inter24) {
+  if (!ctx) return BH_ERR_ARG;
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  if (st) return st;
+  for (int l = 0; l < 24; l++) {
+    if (iters24) iters24[l] = (int64_t)ctx->hstatus->lvl_iters[l];
+    if (active24) active24[l] = (int64_t)ctx->hstatus->lvl_active[l];
+    if (inter24) inter24[l] = (int64_t)ctx->hstatus->lvl_inter[l];
+  }
   return BH_OK;
 }
 

@@ -66,6 +66,11 @@ struct DevStatus {
   uint32_t lvl_count[24];   // internal nodes per level (0..21)
   uint32_t lvl_offset[24];  // exclusive prefix of lvl_count
   uint32_t lvl_cursor[24];
+  // walk statistics per record level (stats mode): group iterations, active
+  // lane-visits, interactions
+  unsigned long long lvl_iters[24];
+  unsigned long long lvl_active[24];
+  unsigned long long lvl_inter[24];
 };
 
 struct __align__(32) Rec {

@@ -143,6 +143,11 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   float ax = 0.f, ay = 0.f, az = 0.f;
   double dax = 0.0, day = 0.0, daz = 0.0;
   bool live = c < Wn;
+  __shared__ unsigned long long s_lv[3][24];
+  if (STATS) {
+    for (int i = threadIdx.x; i < 72; i += blockDim.x) (&s_lv[0][0])[i] = 0ull;
+    __syncthreads();
+  }
   // outer loop: the fp64 fold runs on a uniform exit of the inner loop
   while (G == 32 ? live : __any_sync(full, live)) {
     bool fold;
@@ -160,7 +165,16 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
       const bool acc = ok & (d2 > __uint_as_float(au.x));
       const bool amb = ok & !acc & (d2 >= __uint_as_float(au.y));
       const bool opn = act & !acc & !amb;
-      if (STATS) nop += opn;
+      if (STATS) {
+        nop += opn;
+        const uint32_t lv = au.w & META_LEVEL_MASK;
+        const uint32_t na = __popc(__ballot_sync(full, act) & gmask), ni = __popc(__ballot_sync(full, acc) & gmask);
+        if ((lane & (G - 1)) == 0 && (G == 32 || live)) {
+          atomicAdd(&s_lv[0][lv], (unsigned long long)G);
+          atomicAdd(&s_lv[1][lv], (unsigned long long)na);
+          atomicAdd(&s_lv[2][lv], (unsigned long long)ni);
+        }
+      }
       // interaction, branch-free: f = 0 for lanes that do not accept c
       const float inv = rsqrt_fast(d2 + eps2);
       float f = cm.w * (inv * inv) * inv;
@@ -179,8 +193,12 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
         c = live ? nxt : c;
       }
       live = c < Wn;
+#ifndef BH_NO_FOLD
       fold = acc & ((cnt & 63u) == 0u);
       if (__any_sync(full, fold)) break;
+#else
+      fold = false;
+#endif
       if (G == 32 ? !live : !__any_sync(full, live)) break;
     }
     if (fold) {
@@ -198,6 +216,13 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
     if (STATS) {
       wo += __shfl_xor_sync(full, wo, o);
       wi += __shfl_xor_sync(full, wi, o);
+    }
+  }
+  if (STATS) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 72; i += blockDim.x) {
+      unsigned long long v = (&s_lv[0][0])[i];
+      if (v) atomicAdd(&P.st->lvl_iters[0] + i, v);
     }
   }
   if (lane == 0) {

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--groups", default="32,16,8,4,2,1")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--levels", action="store_true")
     a = ap.parse_args()
     from paper_1109_5190_b200 import BarnesHut
 
@@ -34,6 +35,12 @@ def main():
         bh.compute_forces(_dev_out(bh))
         bh.sync()
         st_stats = bh.get_stats()
+        if a.levels:
+            it, ac, ia = bh.get_walk_level_stats()
+            for l in range(24):
+                if it[l]:
+                    print(f"  level {l:2d}: slots {it[l]:.3e} active {ac[l]/it[l]:.3f} inter {ia[l]/it[l]:.3f} "
+                          f"share-of-slots {it[l]/it.sum():.3f} share-of-inter {ia[l]/ia.sum():.3f}", flush=True)
         bh.set_walk_stats(False)
         bh.sync()
         bh.set_profiling(True)
