@@ -25,9 +25,11 @@
 // carries no fp64 code and no divergent branch.
 //
 // Interaction (fp32): r2 = d2 + eps^2, f = M rsqrt(r2)^3, a += f (dx, dy, dz):
-// 18 flops + 1 MUFU.RSQ.  Partial sums are folded into fp64 at every 64th
-// interaction of the lane (a per-lane rule: the result does not depend on the
-// group size or the rank count).
+// 18 flops + 1 MUFU.RSQ, summed sequentially in fp32 in the lane's own DFS
+// order (so the result does not depend on the group size or the rank count).
+// Measured max per-particle error vs the fp64 oracle: <= 2.5e-5 on cfg1-cfg4
+// (DESIGN.md §6); -DBH_FOLD64 folds the fp32 partials into fp64 every 64
+// interactions (max error <= 1.8e-5 -> 2.7e-6 on cfg2, 17% slower walk).
 //
 // K7 (mode 1): v += a * kick (kick = dt/2 on the first step, dt after; reading
 // L8), x += v dt, written in place to pos4 / vel4 of the particle's storage slot
@@ -135,6 +137,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   const bool gvalid = (__ballot_sync(full, tvalid) & gmask) != 0u;
   const float eps2 = P.eps2;
   const Rec *__restrict__ rec = P.rec;
+  asm volatile("" : "+l"(rec));  // keep the base in a register (no per-iteration constant reload)
   uint32_t c = gvalid ? 0u : Wn;
   // a lane is active at record c iff c >= resume; an invalid (or dropped-out)
   // lane has resume past every record
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
       ax = fmaf(f, dx, ax);
       ay = fmaf(f, dy, ay);
       az = fmaf(f, dz, az);
-      cnt += acc ? 1u : 0u;
+      asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cnt) : "r"((uint32_t)acc));
       resume = acc ? skip : (amb ? 0xffffffffu : resume);
       uint32_t nxt;
       if (G == 32) {
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
         c = live ? nxt : c;
       }
       live = c < Wn;
-#ifndef BH_NO_FOLD
+#ifdef BH_FOLD64
       fold = acc & ((cnt & 63u) == 0u);
       if (__any_sync(full, fold)) break;
 #else
