@@ -250,8 +250,8 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     return BH_ERR_ARG;
   }
   int g = p->walk_group;
-  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32)) {
-    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16 or 32");
+  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || g == 64)) {
+    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16, 32 or 64");
     return BH_ERR_ARG;
   }
   return BH_OK;
@@ -363,8 +363,12 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   memset(&a, 0, sizeof a);
   a.n = n;
   a.buf = ctx->sort_buf;
-  a.group = ctx->p.walk_group ? ctx->p.walk_group : 32;
+  a.group = ctx->p.walk_group;
   a.stats = ctx->walk_stats;
+  // containment test elision (see walk.cu): a cell holding the target has
+  // s/d >= 1/sqrt(3) (d <= sqrt(3) s), so it never passes s/d < theta for
+  // theta < 0.5773; kept with a margin, and only when eps > 0
+  a.need_cont = !(ctx->p.theta < 0.57 && ctx->p.eps > 0.0);
   a.mode = mode;
   a.eps2 = (float)(ctx->p.eps * ctx->p.eps);
   a.G = (float)ctx->p.G;

@@ -143,6 +143,8 @@ struct WalkArgs {
   int buf;              // sort buffer holding vals
   int group;            // lanes per shared traversal
   int stats;            // 1: also count opened nodes and SIMD slots
+  int need_cont;        // 0: theta < 1/sqrt(3) and eps > 0 -> no cell containing the
+                        //    target can pass the MAC and the self record adds 0
   int mode;             // 0 = forces to acc_out (user order), 1 = fused leapfrog
   float eps2, G;
   float kick, dt;       // mode 1

@@ -90,6 +90,13 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
       tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15));
       const double B = (r * (1.0 - delta) - b) / (1.0 + a);
       trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 1e-15)) : -INFINITY;
+      // Levels 20-21: fp32 quantisation can place a particle up to 0.19 grid
+      // quanta outside its key-space cell, so there (and only there) a cell
+      // containing the target could pass s/d < theta for theta < 1/sqrt(3).
+      // The fast walk skips the containment test (walk.cu); never accepting
+      // these cells in the fp32 filter routes every such decision to the exact
+      // re-walk, which tests containment.
+      if (level >= 20) tacc = INFINITY;
     }
     rec[c].aux = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), aux.z, aux.w);
   }

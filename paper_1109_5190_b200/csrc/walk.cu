@@ -242,6 +242,151 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   finish(P, T, dax, day, daz, cnt);
 }
 
+// ---------------------------------------------------------------- k_walk2
+// The production walk: the same per-lane semantics and the same fp32 operation
+// sequence per target as k_walk (bitwise-identical results), but every lane
+// carries TWO targets and does their arithmetic with Blackwell's packed fp32
+// instructions (FADD2 / FMUL2 / FFMA2: one issue slot, two fp32 results; the
+// node's fields enter as broadcast scalar operands).  The record loads, the
+// traversal control and the vote are shared by the pair, so the issue slots per
+// target-visit drop by ~1/3.  A group of GL lanes (2 GL targets, Morton-
+// consecutive) shares one traversal.
+struct F2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ F2 pk2(float lo, float hi) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(F2 a, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
+  F2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+  F2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+  F2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ void fma2_acc(F2 &acc, F2 a, F2 b) {  // acc = a * b + acc, in place
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.v) : "l"(a.v), "l"(b.v));
+}
+
+template <int GL, bool CONT>
+__global__ void __launch_bounds__(256) k_walk2(const WalkParams P) {
+  const uint32_t full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
+  if (P.st->err & ERR_NODE_OVERFLOW) return;
+  const uint32_t Wn = P.st->n_records;
+  // a warp covers 64 consecutive targets; a group of GL lanes covers 2 GL of them
+  const int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2;
+  const int gi = lane / GL, gl = lane % GL;
+  const int64_t tA = wbase + (int64_t)gi * 2 * GL + gl, tB = tA + GL;
+  const bool vA = tA < P.n_targets, vB = tB < P.n_targets;
+  Target TA, TB;
+  if (vA) TA = load_target(P, tA);
+  else { TA.p = 0; TA.Li = 0; TA.s = 0; TA.me = make_float4(0.f, 0.f, 0.f, 0.f); }
+  if (vB) TB = load_target(P, tB);
+  else { TB.p = 0; TB.Li = 0; TB.s = 0; TB.me = make_float4(0.f, 0.f, 0.f, 0.f); }
+  const uint32_t LiA = TA.Li, LiB = TB.Li;
+  const F2 X = pk2(TA.me.x, TB.me.x), Y = pk2(TA.me.y, TB.me.y), Z = pk2(TA.me.z, TB.me.z);
+  const F2 E2 = pk2(P.eps2, P.eps2);
+  const bool gvalid = (__ballot_sync(full, vA || vB) & gmask) != 0u;
+  const Rec *__restrict__ rec = P.rec;
+  uint32_t gmask2 = gmask;
+  asm volatile("" : "+r"(gmask2));  // a plain register: the group test is one LOP3
+  uint32_t c = gvalid ? 0u : Wn;
+  uint32_t resA = vA ? 0u : 0xffffffffu, resB = vB ? 0u : 0xffffffffu;
+  uint32_t cntA = 0, cntB = 0;
+  float ax = 0.f, ay = 0.f, az = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
+  // a finished group parks on the sentinel record Wn (T_acc = T_rej = +inf,
+  // skip = Wn: nothing is accepted or queued there) until the warp is done
+  if (__any_sync(full, c < Wn)) for (;;) {
+    const uint32_t cc = c;
+    const float4 cm = __ldg(&rec[cc].cm);
+    const uint4 au = __ldg(&rec[cc].aux);
+    const uint32_t skip = au.z;
+    const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
+    const F2 DX = sub2(pk2(cm.x, cm.x), X), DY = sub2(pk2(cm.y, cm.y), Y), DZ = sub2(pk2(cm.z, cm.z), Z);
+    const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
+    float d2A, d2B;
+    up2(D2, d2A, d2B);
+    // per-target MAC (identical to k_walk)
+    const bool actA = cc >= resA;
+    const bool actB = cc >= resB;
+    const bool okA = CONT ? actA & !((cc <= LiA) & (skip > LiA)) : actA;
+    const bool okB = CONT ? actB & !((cc <= LiB) & (skip > LiB)) : actB;
+    const bool accA = okA & (d2A > tacc), accB = okB & (d2B > tacc);
+    const bool ambA = okA & !accA & (d2A >= trej), ambB = okB & !accB & (d2B >= trej);
+    const bool opn = (actA & !accA & !ambA) | (actB & !accB & !ambB);
+    // interaction for both targets, branch-free
+    float r2A, r2B;
+    up2(add2(D2, E2), r2A, r2B);
+    const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
+    float fA, fB;
+    up2(mul2(mul2(pk2(cm.w, cm.w), mul2(INV, INV)), INV), fA, fB);
+    fA = accA ? fA : 0.0f;
+    fB = accB ? fB : 0.0f;
+    {  // scalar FFMAs: ptxas keeps loop-carried FFMA2 accumulators with extra moves
+      float dxA, dxB, dyA, dyB, dzA, dzB;
+      up2(DX, dxA, dxB);
+      up2(DY, dyA, dyB);
+      up2(DZ, dzA, dzB);
+      ax = fmaf(fA, dxA, ax);
+      ay = fmaf(fA, dyA, ay);
+      az = fmaf(fA, dzA, az);
+      bx = fmaf(fB, dxB, bx);
+      by = fmaf(fB, dyB, by);
+      bz = fmaf(fB, dzB, bz);
+    }
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cntA) : "r"((uint32_t)accA));
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cntB) : "r"((uint32_t)accB));
+    resA = accA ? skip : (ambA ? 0xffffffffu : resA);
+    resB = accB ? skip : (ambB ? 0xffffffffu : resB);
+    if (GL == 32) {
+      c = __any_sync(full, opn) ? cc + 1u : skip;
+    } else {
+      const uint32_t nxt = (__ballot_sync(full, opn) & gmask2) ? cc + 1u : skip;
+      c = min(nxt, Wn);
+    }
+    if (!__any_sync(full, c < Wn)) break;
+  }
+  if (!CONT) {  // the target's own record was "accepted" with a zero contribution
+    cntA -= vA ? 1u : 0u;
+    cntB -= vB ? 1u : 0u;
+  }
+  const bool redoA = vA && resA == 0xffffffffu, redoB = vB && resB == 0xffffffffu;
+  unsigned long long wc = (redoA ? 0u : cntA) + (redoB ? 0u : cntB);
+  for (int o = 16; o; o >>= 1) wc += __shfl_xor_sync(full, wc, o);
+  if (lane == 0 && wc) {
+    atomicAdd(&P.st->interactions, wc);
+    atomicAdd(&P.st->interactions_cum, wc);
+  }
+  if (vA) {
+    if (redoA) P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)tA;
+    else finish(P, TA, (double)ax, (double)ay, (double)az, cntA);
+  }
+  if (vB) {
+    if (redoB) P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)tB;
+    else finish(P, TB, (double)bx, (double)by, (double)bz, cntB);
+  }
+}
+
 // Exact walk of the queued targets, one lane per target (rare; the fp64 test
 // decides every node the fp32 filter leaves open).
 __global__ void __launch_bounds__(128) k_walk_exact(const WalkParams P) {
@@ -319,6 +464,18 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.theta2 = a.theta2;
   P.own_lo = a.own_lo;
   unsigned grid = (unsigned)((a.n_targets + 255) / 256);
+  if (!a.stats && (a.group == 0 || a.group == 64)) {
+    // production path: 2 targets per lane (packed fp32), 32- or 64-target groups
+    const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
+    const bool cont = a.need_cont;
+    if (a.group == 64) {
+      if (cont) k_walk2<32, true><<<grid2, 256, 0, s>>>(P);
+      else k_walk2<32, false><<<grid2, 256, 0, s>>>(P);
+    } else {
+      if (cont) k_walk2<16, true><<<grid2, 256, 0, s>>>(P);
+      else k_walk2<16, false><<<grid2, 256, 0, s>>>(P);
+    }
+  } else {
 #define BH_WALK_CASE(g)                                                     \
   case g:                                                                   \
     if (a.stats) k_walk<g, true><<<grid, 256, 0, s>>>(P);                   \
@@ -334,6 +491,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
     BH_WALK_CASE(32)
   }
 #undef BH_WALK_CASE
+  }
   // the exact re-walk: a fixed grid, grid-stride over the device-side queue
   int64_t eg = (a.n_targets + 127) / 128;
   if (eg > 148 * 4) eg = 148 * 4;
