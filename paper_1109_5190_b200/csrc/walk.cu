@@ -321,6 +321,11 @@ __global__ void __launch_bounds__(256) k_walk2(const WalkParams P) {
     const float4 cm = __ldg(&rec[cc].cm);
     const uint4 au = __ldg(&rec[cc].aux);
     const uint32_t skip = au.z;
+#ifndef BH_NO_PREFETCH
+    // the next record is c + 1 or skip(c): start pulling skip's line into L1
+    // while this record's MAC and interaction are computed
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + skip));
+#endif
     const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
     const F2 DX = sub2(pk2(cm.x, cm.x), X), DY = sub2(pk2(cm.y, cm.y), Y), DZ = sub2(pk2(cm.z, cm.z), Z);
     const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
