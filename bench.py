@@ -196,8 +196,9 @@ def ours_arm(args):
     import torch.distributed as dist
 
     from paper_1109_5190_b200 import BarnesHut, bh as bhmod
+    from paper_1109_5190_b200 import dist as bdist
 
-    rank, world, local = env_rank()
+    rank, world, local = bdist.env_rank()
     if world != args.gpus and not (world == 1 and args.gpus == 1):
         print(f"--gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     device = local if world > 1 else 0
@@ -205,9 +206,8 @@ def ours_arm(args):
     comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
-        uid = [bhmod.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = bhmod.nccl_comm_init(uid[0], world, rank, device)
+        uid = bdist.share_nccl_id(bhmod.nccl_unique_id, dist)
+        comm = bhmod.nccl_comm_init(uid, world, rank, device)
     cfg = bhgen.CONFIGS[args.config]
     m, p, v = bhgen.generate(cfg)
     prm = bhgen.params(cfg)
@@ -224,9 +224,7 @@ def ours_arm(args):
     def allreduce(x, op):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
-        dist.all_reduce(t, op=op)
-        return float(t.item())
+        return bdist.reduce_scalar(x, dist, "max" if op == dist.ReduceOp.MAX else "sum", device=f"cuda:{device}")
 
     # warm-up (untimed)
     bh.step(args.warmup)

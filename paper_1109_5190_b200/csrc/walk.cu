@@ -286,8 +286,11 @@ __device__ __forceinline__ void fma2_acc(F2 &acc, F2 a, F2 b) {  // acc = a * b 
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.v) : "l"(a.v), "l"(b.v));
 }
 
+#ifndef BH_WALK2_MINB
+#define BH_WALK2_MINB 1
+#endif
 template <int GL, bool CONT>
-__global__ void __launch_bounds__(256) k_walk2(const WalkParams P) {
+__global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P) {
   const uint32_t full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(256) k_walk2(const WalkParams P) {
     const float4 cm = __ldg(&rec[cc].cm);
     const uint4 au = __ldg(&rec[cc].aux);
     const uint32_t skip = au.z;
-#ifndef BH_NO_PREFETCH
+#ifdef BH_PREFETCH_SKIP
     // the next record is c + 1 or skip(c): start pulling skip's line into L1
     // while this record's MAC and interaction are computed
     asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + skip));
