@@ -289,34 +289,52 @@ __device__ __forceinline__ void fma2_acc(F2 &acc, F2 a, F2 b) {  // acc = a * b 
 #ifndef BH_WALK2_MINB
 #define BH_WALK2_MINB 1
 #endif
-template <int GL, bool CONT>
+// NP pairs of targets per lane (2 NP targets), GL lanes per group: a group of
+// 2 NP GL Morton-consecutive targets shares one traversal.
+template <int GL, int NP, bool CONT>
 __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P) {
+  constexpr int TPL = 2 * NP;  // targets per lane
   const uint32_t full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
   if (P.st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t Wn = P.st->n_records;
-  // a warp covers 64 consecutive targets; a group of GL lanes covers 2 GL of them
-  const int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2;
+  const int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * TPL;
   const int gi = lane / GL, gl = lane % GL;
-  const int64_t tA = wbase + (int64_t)gi * 2 * GL + gl, tB = tA + GL;
-  const bool vA = tA < P.n_targets, vB = tB < P.n_targets;
-  Target TA, TB;
-  if (vA) TA = load_target(P, tA);
-  else { TA.p = 0; TA.Li = 0; TA.s = 0; TA.me = make_float4(0.f, 0.f, 0.f, 0.f); }
-  if (vB) TB = load_target(P, tB);
-  else { TB.p = 0; TB.Li = 0; TB.s = 0; TB.me = make_float4(0.f, 0.f, 0.f, 0.f); }
-  const uint32_t LiA = TA.Li, LiB = TB.Li;
-  const F2 X = pk2(TA.me.x, TB.me.x), Y = pk2(TA.me.y, TB.me.y), Z = pk2(TA.me.z, TB.me.z);
+  const int64_t tbase = wbase + (int64_t)gi * TPL * GL + gl;
+  Target T[TPL];
+  bool v[TPL];
+  bool anyv = false;
+#pragma unroll
+  for (int k = 0; k < TPL; k++) {
+    const int64_t t = tbase + (int64_t)k * GL;
+    v[k] = t < P.n_targets;
+    anyv |= v[k];
+    if (v[k]) T[k] = load_target(P, t);
+    else { T[k].p = 0; T[k].Li = 0; T[k].s = 0; T[k].me = make_float4(0.f, 0.f, 0.f, 0.f); }
+  }
+  uint32_t Li[TPL], res[TPL], cnt[TPL];
+  float ax[TPL], ay[TPL], az[TPL];
+  F2 X[NP], Y[NP], Z[NP];
+#pragma unroll
+  for (int k = 0; k < TPL; k++) {
+    Li[k] = T[k].Li;
+    res[k] = v[k] ? 0u : 0xffffffffu;
+    cnt[k] = 0;
+    ax[k] = ay[k] = az[k] = 0.f;
+  }
+#pragma unroll
+  for (int j = 0; j < NP; j++) {
+    X[j] = pk2(T[2 * j].me.x, T[2 * j + 1].me.x);
+    Y[j] = pk2(T[2 * j].me.y, T[2 * j + 1].me.y);
+    Z[j] = pk2(T[2 * j].me.z, T[2 * j + 1].me.z);
+  }
   const F2 E2 = pk2(P.eps2, P.eps2);
-  const bool gvalid = (__ballot_sync(full, vA || vB) & gmask) != 0u;
+  const bool gvalid = (__ballot_sync(full, anyv) & gmask) != 0u;
   const Rec *__restrict__ rec = P.rec;
   uint32_t gmask2 = gmask;
   asm volatile("" : "+r"(gmask2));  // a plain register: the group test is one LOP3
   uint32_t c = gvalid ? 0u : Wn;
-  uint32_t resA = vA ? 0u : 0xffffffffu, resB = vB ? 0u : 0xffffffffu;
-  uint32_t cntA = 0, cntB = 0;
-  float ax = 0.f, ay = 0.f, az = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
   // a finished group parks on the sentinel record Wn (T_acc = T_rej = +inf,
   // skip = Wn: nothing is accepted or queued there) until the warp is done
   if (__any_sync(full, c < Wn)) for (;;) {
@@ -324,48 +342,44 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
     const float4 cm = __ldg(&rec[cc].cm);
     const uint4 au = __ldg(&rec[cc].aux);
     const uint32_t skip = au.z;
-#ifdef BH_PREFETCH_SKIP
-    // the next record is c + 1 or skip(c): start pulling skip's line into L1
-    // while this record's MAC and interaction are computed
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + skip));
-#endif
     const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
-    const F2 DX = sub2(pk2(cm.x, cm.x), X), DY = sub2(pk2(cm.y, cm.y), Y), DZ = sub2(pk2(cm.z, cm.z), Z);
-    const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
-    float d2A, d2B;
-    up2(D2, d2A, d2B);
-    // per-target MAC (identical to k_walk)
-    const bool actA = cc >= resA;
-    const bool actB = cc >= resB;
-    const bool okA = CONT ? actA & !((cc <= LiA) & (skip > LiA)) : actA;
-    const bool okB = CONT ? actB & !((cc <= LiB) & (skip > LiB)) : actB;
-    const bool accA = okA & (d2A > tacc), accB = okB & (d2B > tacc);
-    const bool ambA = okA & !accA & (d2A >= trej), ambB = okB & !accB & (d2B >= trej);
-    const bool opn = (actA & !accA & !ambA) | (actB & !accB & !ambB);
-    // interaction for both targets, branch-free
-    float r2A, r2B;
-    up2(add2(D2, E2), r2A, r2B);
-    const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
-    float fA, fB;
-    up2(mul2(mul2(pk2(cm.w, cm.w), mul2(INV, INV)), INV), fA, fB);
-    fA = accA ? fA : 0.0f;
-    fB = accB ? fB : 0.0f;
-    {  // scalar FFMAs: ptxas keeps loop-carried FFMA2 accumulators with extra moves
-      float dxA, dxB, dyA, dyB, dzA, dzB;
-      up2(DX, dxA, dxB);
-      up2(DY, dyA, dyB);
-      up2(DZ, dzA, dzB);
-      ax = fmaf(fA, dxA, ax);
-      ay = fmaf(fA, dyA, ay);
-      az = fmaf(fA, dzA, az);
-      bx = fmaf(fB, dxB, bx);
-      by = fmaf(fB, dyB, by);
-      bz = fmaf(fB, dzB, bz);
+    bool opn = false;
+#pragma unroll
+    for (int j = 0; j < NP; j++) {
+      const int a = 2 * j, b = 2 * j + 1;
+      const F2 DX = sub2(pk2(cm.x, cm.x), X[j]), DY = sub2(pk2(cm.y, cm.y), Y[j]),
+               DZ = sub2(pk2(cm.z, cm.z), Z[j]);
+      const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
+      float d2A, d2B;
+      up2(D2, d2A, d2B);
+      // per-target MAC (identical decisions to k_walk)
+      const bool actA = cc >= res[a], actB = cc >= res[b];
+      const bool okA = CONT ? actA & !((cc <= Li[a]) & (skip > Li[a])) : actA;
+      const bool okB = CONT ? actB & !((cc <= Li[b]) & (skip > Li[b])) : actB;
+      const bool accA = okA & (d2A > tacc), accB = okB & (d2B > tacc);
+      // inconclusive fp32 test: the target drops out (resume = ~0) and is
+      // re-walked with the exact fp64 test by k_walk_exact
+      const bool ambA = okA & !accA & (d2A >= trej), ambB = okB & !accB & (d2B >= trej);
+      opn |= (actA & !accA & !ambA) | (actB & !accB & !ambB);
+      // interaction for both targets of the pair, branch-free
+      float r2A, r2B;
+      up2(add2(D2, E2), r2A, r2B);
+      const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
+      float fA, fB;
+      up2(mul2(mul2(pk2(cm.w, cm.w), mul2(INV, INV)), INV), fA, fB);
+      const F2 FF = pk2(accA ? fA : 0.0f, accB ? fB : 0.0f);
+      // packed accumulate on (a, b) register pairs (this form avoids ptxas moves)
+      asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+          : "+f"(ax[a]), "+f"(ax[b]) : "l"(FF.v), "l"(DX.v));
+      asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+          : "+f"(ay[a]), "+f"(ay[b]) : "l"(FF.v), "l"(DY.v));
+      asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+          : "+f"(az[a]), "+f"(az[b]) : "l"(FF.v), "l"(DZ.v));
+      asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cnt[a]) : "r"((uint32_t)accA));
+      asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cnt[b]) : "r"((uint32_t)accB));
+      res[a] = accA ? skip : (ambA ? 0xffffffffu : res[a]);
+      res[b] = accB ? skip : (ambB ? 0xffffffffu : res[b]);
     }
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cntA) : "r"((uint32_t)accA));
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cntB) : "r"((uint32_t)accB));
-    resA = accA ? skip : (ambA ? 0xffffffffu : resA);
-    resB = accB ? skip : (ambB ? 0xffffffffu : resB);
     if (GL == 32) {
       c = __any_sync(full, opn) ? cc + 1u : skip;
     } else {
@@ -374,24 +388,24 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
     }
     if (!__any_sync(full, c < Wn)) break;
   }
-  if (!CONT) {  // the target's own record was "accepted" with a zero contribution
-    cntA -= vA ? 1u : 0u;
-    cntB -= vB ? 1u : 0u;
+  unsigned long long wc = 0;
+  bool redo[TPL];
+#pragma unroll
+  for (int k = 0; k < TPL; k++) {
+    redo[k] = v[k] && res[k] == 0xffffffffu;
+    if (!CONT) cnt[k] -= v[k] ? 1u : 0u;  // own record: "accepted", zero contribution
+    wc += redo[k] ? 0u : cnt[k];
   }
-  const bool redoA = vA && resA == 0xffffffffu, redoB = vB && resB == 0xffffffffu;
-  unsigned long long wc = (redoA ? 0u : cntA) + (redoB ? 0u : cntB);
   for (int o = 16; o; o >>= 1) wc += __shfl_xor_sync(full, wc, o);
   if (lane == 0 && wc) {
     atomicAdd(&P.st->interactions, wc);
     atomicAdd(&P.st->interactions_cum, wc);
   }
-  if (vA) {
-    if (redoA) P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)tA;
-    else finish(P, TA, (double)ax, (double)ay, (double)az, cntA);
-  }
-  if (vB) {
-    if (redoB) P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)tB;
-    else finish(P, TB, (double)bx, (double)by, (double)bz, cntB);
+#pragma unroll
+  for (int k = 0; k < TPL; k++) {
+    if (!v[k]) continue;
+    if (redo[k]) P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)(tbase + (int64_t)k * GL);
+    else finish(P, T[k], (double)ax[k], (double)ay[k], (double)az[k], cnt[k]);
   }
 }
 
@@ -472,16 +486,25 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.theta2 = a.theta2;
   P.own_lo = a.own_lo;
   unsigned grid = (unsigned)((a.n_targets + 255) / 256);
-  if (!a.stats && (a.group == 0 || a.group == 64)) {
-    // production path: 2 targets per lane (packed fp32), 32- or 64-target groups
-    const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
+  if (!a.stats && (a.group == 0 || a.group == 64 || a.group == 65)) {
+    // production path: packed fp32 pairs of targets per lane
+    //   0 : 16 lanes x 2 targets (32-target groups)   [default]
+    //   64: 32 lanes x 2 targets (64-target groups)
+    //   65: 8 lanes x 4 targets (32-target groups)
     const bool cont = a.need_cont;
-    if (a.group == 64) {
-      if (cont) k_walk2<32, true><<<grid2, 256, 0, s>>>(P);
-      else k_walk2<32, false><<<grid2, 256, 0, s>>>(P);
+    if (a.group == 65) {
+      const unsigned g4 = (unsigned)((a.n_targets + 1023) / 1024);
+      if (cont) k_walk2<8, 2, true><<<g4, 256, 0, s>>>(P);
+      else k_walk2<8, 2, false><<<g4, 256, 0, s>>>(P);
     } else {
-      if (cont) k_walk2<16, true><<<grid2, 256, 0, s>>>(P);
-      else k_walk2<16, false><<<grid2, 256, 0, s>>>(P);
+      const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
+      if (a.group == 64) {
+        if (cont) k_walk2<32, 1, true><<<grid2, 256, 0, s>>>(P);
+        else k_walk2<32, 1, false><<<grid2, 256, 0, s>>>(P);
+      } else {
+        if (cont) k_walk2<16, 1, true><<<grid2, 256, 0, s>>>(P);
+        else k_walk2<16, 1, false><<<grid2, 256, 0, s>>>(P);
+      }
     }
   } else {
 #define BH_WALK_CASE(g)                                                     \
