@@ -287,7 +287,7 @@ __device__ __forceinline__ void fma2_acc(F2 &acc, F2 a, F2 b) {  // acc = a * b 
 }
 
 #ifndef BH_WALK2_MINB
-#define BH_WALK2_MINB 1
+#define BH_WALK2_MINB 5
 #endif
 // NP pairs of targets per lane (2 NP targets), GL lanes per group: a group of
 // 2 NP GL Morton-consecutive targets shares one traversal.
