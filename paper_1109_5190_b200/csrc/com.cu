@@ -18,12 +18,12 @@
 //   otherwise the walk re-evaluates the exact fp64 test of the oracle.
 // With r = s_l / theta the exact test is d > r (s^2 < theta^2 d^2).  The fp32
 // distance of the walk differs from the oracle's fp64 distance by at most
-//   |d32 - d| <= 2u d + 2u |c32|   (u = 2^-24: com rounding + subtraction)
-// and the fp32 sum of squares by a relative 8u; delta = 1e-12 covers the
-// oracle's own fp64 rounding.  Hence (safety factor 2 on every term)
+//   |d32 - d| <= u d + u(1+u) |c32|   (u = 2^-24: subtraction + com rounding)
+// and the fp32 sum of squares (mul, fma, fma) by a relative 3u; delta = 1e-12
+// covers the oracle's own fp64 rounding.  Hence (safety factor 1.5 on each term)
 //   T_acc = RU(((r(1+delta) + b) / (1-a))^2 (1+g)),
 //   T_rej = RD(((r(1-delta) - b) / (1+a))^2 (1-g))   (or -inf if negative),
-// with a = 2u, b = 2u |c32| 1.001, g = 8u.  theta == 0: T_acc = T_rej = +inf.
+// with a = 1.5u, b = 1.5u |c32|, g = 4.5u.  theta == 0: T_acc = T_rej = +inf.
 #include <math.h>
 
 #include "bh_internal.cuh"
@@ -85,7 +85,10 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
       const double s = ldexp(Ld, -level);
       const double r = s / theta;
       const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
-      const double a = 2.0 * u, b = 2.0 * u * C * 1.001, g = 8.0 * u, delta = 1e-12;
+      // first-order bounds (u: com rounding |c32 - c64| <= u(1+u)|c32|, one
+      // rounding of the subtraction, <= 3 roundings in the fp32 sum of squares)
+      // with a safety factor 1.5 on every term
+      const double a = 1.5 * u, b = 1.5 * u * C, g = 4.5 * u, delta = 1e-12;
       const double A = (r * (1.0 + delta) + b) / (1.0 - a);
       tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15));
       const double B = (r * (1.0 - delta) - b) / (1.0 + a);
