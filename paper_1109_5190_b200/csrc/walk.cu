@@ -409,54 +409,138 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
   }
 }
 
-// Exact walk of the queued targets, one lane per target (rare; the fp64 test
-// decides every node the fp32 filter leaves open).
-__global__ void __launch_bounds__(128) k_walk_exact(const WalkParams P) {
+// Exact walk of the queued targets.  One WARP per target: the node set a target
+// interacts with does not depend on the visiting order, so the warp expands the
+// target's frontier 32 nodes at a time from a LIFO stack in shared memory
+// (opened nodes push their children in a fixed, ballot-ranked order) and tests
+// each node with the fp32 filter, falling back to the oracle's fp64 formula on
+// the ambiguous ones.  Partial sums: fp64 per lane, reduced in lane order.  A
+// stack overflow (never seen; bounded by ~8 x depth x 32) falls back to the
+// one-lane DFS below.
+constexpr int EXACT_WARPS = 4;
+constexpr int EXACT_STACK = 2048;
+
+__device__ void exact_dfs_one_lane(const WalkParams &P, const Target &T, uint32_t Wn, double Ld, double &dax,
+                                   double &day, double &daz, uint32_t &cnt, uint32_t &fb, uint32_t &nop) {
+  uint32_t c = 0;
+  while (c < Wn) {
+    const float4 cm = P.rec[c].cm;
+    const uint4 au = P.rec[c].aux;
+    const float dx = cm.x - T.me.x, dy = cm.y - T.me.y, dz = cm.z - T.me.z;
+    const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    const bool cont = (c <= T.Li) & (au.z > T.Li);
+    bool acc = !cont & (d2 > __uint_as_float(au.x));
+    if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
+      acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
+      fb++;
+    }
+    if (acc) {
+      const float inv = rsqrt_fast(d2 + P.eps2);
+      const float f = cm.w * (inv * inv) * inv;
+      dax += (double)(f * dx);
+      day += (double)(f * dy);
+      daz += (double)(f * dz);
+      cnt++;
+      c = au.z;
+    } else {
+      nop++;
+      c = c + 1u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * EXACT_WARPS) k_walk_exact(const WalkParams P) {
+  __shared__ uint32_t stack[EXACT_WARPS][EXACT_STACK];
   if (P.st->err & ERR_NODE_OVERFLOW) return;
+  const uint32_t full = 0xffffffffu;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t *stk = stack[w];
   const uint32_t Wn = P.st->n_records;
   const unsigned long long nredo = P.st->n_redo;
   const double Ld = (double)P.st->L;
-  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < nredo;
-       k += (unsigned long long)gridDim.x * blockDim.x) {
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  for (unsigned long long k = blockIdx.x * (unsigned long long)EXACT_WARPS + w; k < nredo;
+       k += (unsigned long long)gridDim.x * EXACT_WARPS) {
     const Target T = load_target(P, P.redo[k]);
-    uint32_t c = 0, cnt = 0, fb = 0, nop = 0;
-    float ax = 0.f, ay = 0.f, az = 0.f;
     double dax = 0.0, day = 0.0, daz = 0.0;
-    while (c < Wn) {
-      const float4 cm = P.rec[c].cm;
-      const uint4 au = P.rec[c].aux;
-      const float dx = cm.x - T.me.x, dy = cm.y - T.me.y, dz = cm.z - T.me.z;
-      const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const bool cont = (c <= T.Li) & (au.z > T.Li);
-      bool acc = !cont & (d2 > __uint_as_float(au.x));
-      if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
-        acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
-        fb++;
-      }
-      if (acc) {
-        const float inv = rsqrt_fast(d2 + P.eps2);
-        const float f = cm.w * (inv * inv) * inv;
-        ax = fmaf(f, dx, ax);
-        ay = fmaf(f, dy, ay);
-        az = fmaf(f, dz, az);
-        cnt++;
-        if ((cnt & 63u) == 0u) {
-          dax += ax; day += ay; daz += az;
-          ax = ay = az = 0.f;
+    uint32_t cnt = 0, fb = 0, nop = 0;
+    uint32_t sp = 1;
+    if (lane == 0) stk[0] = 0u;  // the root
+    bool overflow = false;
+    __syncwarp();
+    while (sp > 0 && !overflow) {
+      const uint32_t nt = sp < 32u ? sp : 32u;
+      const uint32_t base = sp - nt;
+      const bool have = (uint32_t)lane < nt;
+      const uint32_t c = have ? stk[base + lane] : 0u;
+      __syncwarp();
+      sp = base;
+      bool opn = false;
+      uint32_t skip = 0;
+      if (have) {
+        const float4 cm = P.rec[c].cm;
+        const uint4 au = P.rec[c].aux;
+        skip = au.z;
+        const float dx = cm.x - T.me.x, dy = cm.y - T.me.y, dz = cm.z - T.me.z;
+        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const bool cont = (c <= T.Li) & (au.z > T.Li);
+        bool acc = !cont & (d2 > __uint_as_float(au.x));
+        if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
+          acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
+          fb++;
         }
-        c = au.z;
-      } else {
-        nop++;
-        c = c + 1u;
+        if (acc) {
+          const float inv = rsqrt_fast(d2 + P.eps2);
+          const float f = cm.w * (inv * inv) * inv;
+          dax += (double)(f * dx);
+          day += (double)(f * dy);
+          daz += (double)(f * dz);
+          cnt++;
+        } else {
+          nop++;
+          opn = skip > c + 1u;  // has children
+        }
       }
+      // push the children of every opened node, one child per lane per round,
+      // at ballot-ranked positions (deterministic order)
+      uint32_t ch = c + 1u;
+      for (;;) {
+        const bool push = opn && ch < skip;
+        const uint32_t b = __ballot_sync(full, push);
+        if (!b) break;
+        if (sp + __popc(b) > EXACT_STACK) { overflow = true; break; }
+        if (push) {
+          stk[sp + __popc(b & lt)] = ch;
+          ch = P.rec[ch].aux.z;
+        }
+        sp += __popc(b);
+      }
+      __syncwarp();
     }
-    dax += ax; day += ay; daz += az;
-    atomicAdd(&P.st->interactions, (unsigned long long)cnt);
-    atomicAdd(&P.st->interactions_cum, (unsigned long long)cnt);
-    atomicAdd(&P.st->fallbacks, (unsigned long long)fb);
-    atomicAdd(&P.st->opens, (unsigned long long)nop);
-    atomicAdd(&P.st->opens_cum, (unsigned long long)nop);
-    finish(P, T, dax, day, daz, cnt);
+    // reduce the lane partials in lane order
+    for (int o = 16; o; o >>= 1) {
+      dax += __shfl_xor_sync(full, dax, o);
+      day += __shfl_xor_sync(full, day, o);
+      daz += __shfl_xor_sync(full, daz, o);
+      cnt += __shfl_xor_sync(full, cnt, o);
+      fb += __shfl_xor_sync(full, fb, o);
+      nop += __shfl_xor_sync(full, nop, o);
+    }
+    if (overflow) {  // lane 0 redoes the target depth-first
+      dax = day = daz = 0.0;
+      cnt = fb = nop = 0;
+      if (lane == 0) exact_dfs_one_lane(P, T, Wn, Ld, dax, day, daz, cnt, fb, nop);
+    }
+    if (lane == 0) {
+      atomicAdd(&P.st->interactions, (unsigned long long)cnt);
+      atomicAdd(&P.st->interactions_cum, (unsigned long long)cnt);
+      atomicAdd(&P.st->fallbacks, (unsigned long long)fb);
+      atomicAdd(&P.st->opens, (unsigned long long)nop);
+      atomicAdd(&P.st->opens_cum, (unsigned long long)nop);
+      finish(P, T, dax, day, daz, cnt);
+    }
+    __syncwarp();
   }
 }
 
@@ -523,10 +607,10 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   }
 #undef BH_WALK_CASE
   }
-  // the exact re-walk: a fixed grid, grid-stride over the device-side queue
-  int64_t eg = (a.n_targets + 127) / 128;
-  if (eg > 148 * 4) eg = 148 * 4;
-  k_walk_exact<<<(unsigned)eg, 128, 0, s>>>(P);
+  // the exact re-walk: a fixed grid of warps, grid-stride over the device-side queue
+  int64_t eg = (a.n_targets + EXACT_WARPS - 1) / EXACT_WARPS;
+  if (eg > 148 * 8) eg = 148 * 8;
+  k_walk_exact<<<(unsigned)eg, 32 * EXACT_WARPS, 0, s>>>(P);
   return cudaGetLastError();
 }
 
