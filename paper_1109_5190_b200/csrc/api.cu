@@ -37,6 +37,8 @@ struct bh_ctx {
   bool tree_valid;
   bool walked;
   int walk_stats;
+  int sm_local;
+  int num_sms;
   int sort_buf;
   DevStatus *hstatus;  // pinned
   cudaEvent_t status_ev;
@@ -365,6 +367,8 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.buf = ctx->sort_buf;
   a.group = ctx->p.walk_group;
   a.stats = ctx->walk_stats;
+  a.sm_local = ctx->sm_local;
+  a.num_sms = ctx->num_sms;
   // containment test elision (see walk.cu): a cell holding the target has
   // s/d >= 1/sqrt(3) (d <= sqrt(3) s), so it never passes s/d < theta for
   // theta < 0.5773; kept with a margin, and only when eps > 0
@@ -492,11 +496,15 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->tree_valid = false;
   ctx->walked = false;
   ctx->walk_stats = 0;
+  ctx->sm_local = getenv("BH_SM_LOCAL") ? atoi(getenv("BH_SM_LOCAL")) : 1;
+  ctx->num_sms = 148;
   ctx->sort_buf = 0;
   ctx->status_pending = false;
   bh_status st = BH_OK;
   do {
     if (cudaSetDevice(p->device) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "cudaSetDevice(%d) failed", p->device); break; }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+    if (ctx->num_sms < 1 || ctx->num_sms > 256) ctx->num_sms = 148;
     if (p->stream) {
       ctx->stream = (cudaStream_t)p->stream;
       ctx->own_stream = false;

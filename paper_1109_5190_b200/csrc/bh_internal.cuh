@@ -57,6 +57,7 @@ struct DevStatus {
   unsigned long long opens;          // last walk: MAC tests that opened a node (incl. self leaf)
   unsigned long long iters;          // last walk: group-loop iterations summed over lanes
   unsigned long long n_redo;         // last walk: targets re-walked with the exact fp64 MAC
+  uint32_t sm_next[256];             // walk: next chunk of each SM's segment (zeroed per walk)
   unsigned long long interactions_cum;  // since create / set_state
   unsigned long long opens_cum;
   float lo[3];
@@ -143,6 +144,8 @@ struct WalkArgs {
   int buf;              // sort buffer holding vals
   int group;            // lanes per shared traversal
   int stats;            // 1: also count opened nodes and SIMD slots
+  int sm_local;         // 1: SM-local chunk scheduling of the walk (see walk.cu)
+  int num_sms;
   int need_cont;        // 0: theta < 1/sqrt(3) and eps > 0 -> no cell containing the
                         //    target can pass the MAC and the self record adds 0
   int mode;             // 0 = forces to acc_out (user order), 1 = fused leapfrog

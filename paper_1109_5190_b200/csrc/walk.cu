@@ -60,6 +60,8 @@ struct WalkParams {
   float eps2, G, kick, dt;
   double theta2;
   uint32_t own_lo;
+  int sm_local, num_sms;
+  uint32_t n_chunks;  // walk: chunks of 2 NP x 256 targets
 };
 
 __device__ __forceinline__ float rsqrt_fast(float x) {
@@ -299,7 +301,32 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
   const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
   if (P.st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t Wn = P.st->n_records;
-  const int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * TPL;
+  // SM-local scheduling: the chunks (one block's targets) are split into one
+  // contiguous Morton segment per SM; a block takes the next chunk of its SM's
+  // segment (so the blocks resident on an SM walk neighbouring regions and share
+  // L1), or steals from the following segments once its own is done.  Every
+  // block claims exactly one chunk and there are as many blocks as chunks.
+  uint32_t chunk = blockIdx.x;
+  if (P.sm_local) {
+    __shared__ uint32_t s_chunk;
+    if (threadIdx.x == 0) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      const uint32_t ns = (uint32_t)P.num_sms;
+      sm %= ns;
+      for (uint32_t k = 0;; k++) {
+        const uint32_t seg = (sm + k) % ns;
+        const uint32_t lo = (uint32_t)((unsigned long long)P.n_chunks * seg / ns);
+        const uint32_t hi = (uint32_t)((unsigned long long)P.n_chunks * (seg + 1) / ns);
+        if (lo == hi) continue;
+        const uint32_t got = atomicAdd(&P.st->sm_next[seg], 1u);
+        if (lo + got < hi) { s_chunk = lo + got; break; }
+      }
+    }
+    __syncthreads();
+    chunk = s_chunk;
+  }
+  const int64_t wbase = (chunk * (int64_t)blockDim.x + (threadIdx.x & ~31)) * TPL;
   const int gi = lane / GL, gl = lane % GL;
   const int64_t tbase = wbase + (int64_t)gi * TPL * GL + gl;
   Target T[TPL];
@@ -569,6 +596,12 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.dt = a.dt;
   P.theta2 = a.theta2;
   P.own_lo = a.own_lo;
+  P.sm_local = a.sm_local;
+  P.num_sms = a.num_sms > 0 ? a.num_sms : 148;
+  if (P.sm_local) {
+    cudaError_t e = cudaMemsetAsync(W.status->sm_next, 0, sizeof(W.status->sm_next), s);
+    if (e != cudaSuccess) return e;
+  }
   unsigned grid = (unsigned)((a.n_targets + 255) / 256);
   if (!a.stats && (a.group == 0 || a.group == 64 || a.group == 65)) {
     // production path: packed fp32 pairs of targets per lane
@@ -578,10 +611,12 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
     const bool cont = a.need_cont;
     if (a.group == 65) {
       const unsigned g4 = (unsigned)((a.n_targets + 1023) / 1024);
+      P.n_chunks = g4;
       if (cont) k_walk2<8, 2, true><<<g4, 256, 0, s>>>(P);
       else k_walk2<8, 2, false><<<g4, 256, 0, s>>>(P);
     } else {
       const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
+      P.n_chunks = grid2;
       if (a.group == 64) {
         if (cont) k_walk2<32, 1, true><<<grid2, 256, 0, s>>>(P);
         else k_walk2<32, 1, false><<<grid2, 256, 0, s>>>(P);
