@@ -496,7 +496,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->tree_valid = false;
   ctx->walked = false;
   ctx->walk_stats = 0;
-  ctx->sm_local = getenv("BH_SM_LOCAL") ? atoi(getenv("BH_SM_LOCAL")) : 1;
+  ctx->sm_local = getenv("BH_SM_LOCAL") ? atoi(getenv("BH_SM_LOCAL")) : 0;
   ctx->num_sms = 148;
   ctx->sort_buf = 0;
   ctx->status_pending = false;
