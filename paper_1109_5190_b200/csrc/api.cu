@@ -38,6 +38,8 @@ struct bh_ctx {
   bool walked;
   int walk_stats;
   int sm_local;
+  int use_graphs;
+  cudaGraphExec_t step_graph[2];  // [0]: half kick (first step), [1]: full kick
   int num_sms;
   int sort_buf;
   DevStatus *hstatus;  // pinned
@@ -496,6 +498,8 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->tree_valid = false;
   ctx->walked = false;
   ctx->walk_stats = 0;
+  ctx->use_graphs = getenv("BH_NO_GRAPHS") ? 0 : 1;
+  ctx->step_graph[0] = ctx->step_graph[1] = nullptr;
   ctx->sm_local = getenv("BH_SM_LOCAL") ? atoi(getenv("BH_SM_LOCAL")) : 0;
   ctx->num_sms = 148;
   ctx->sort_buf = 0;
@@ -613,6 +617,52 @@ bh_status bh_compute_forces(bh_ctx *ctx, float *acc, int where) {
   return BH_OK;
 }
 
+// one time step's launches (K0-K8) on ctx->stream
+static bh_status enqueue_step(bh_ctx *ctx, float kick) {
+  bh_status st = build_tree(ctx);
+  if (st) return st;
+  st = walk(ctx, 1, kick, nullptr, false);
+  if (st) return st;
+  return exchange(ctx);
+}
+
+static void drop_graphs(bh_ctx *ctx) {
+  for (int i = 0; i < 2; i++)
+    if (ctx->step_graph[i]) {
+      cudaGraphExecDestroy(ctx->step_graph[i]);
+      ctx->step_graph[i] = nullptr;
+    }
+}
+
+// The step is a fixed sequence of ~45 launches whose sizes do not depend on the
+// data (every kernel reads its counts from the device), so it is captured once
+// per kick value into a CUDA graph and replayed: one launch per step instead of
+// ~45 (matters for the small configurations).  Not used while profiling (the
+// per-phase events) or for multi-rank communicators.
+static bh_status step_graph(bh_ctx *ctx, int which, float kick, cudaGraphExec_t *out) {
+  if (ctx->step_graph[which]) {
+    *out = ctx->step_graph[which];
+    return BH_OK;
+  }
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  bh_status st = enqueue_step(ctx, kick);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (st) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(ctx, BH_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&ctx->step_graph[which], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    ctx->step_graph[which] = nullptr;
+    return fail(ctx, BH_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+  }
+  *out = ctx->step_graph[which];
+  return BH_OK;
+}
+
 bh_status bh_step(bh_ctx *ctx, int nsteps) {
   if (!ctx || nsteps < 0) return fail(ctx, BH_ERR_ARG, "bad arguments");
   bh_status st = set_dev(ctx);
@@ -622,15 +672,21 @@ bh_status bh_step(bh_ctx *ctx, int nsteps) {
     st = status_from_device(ctx);
     if (st) return st;
   }
+  const bool graphs = ctx->use_graphs && !ctx->prof && !(ctx->p.world > 1 && ctx->p.nccl_comm);
   for (int k = 0; k < nsteps; k++) {
     if (ctx->prof) ctx->prof_calls++;
-    st = build_tree(ctx);
-    if (st) return st;
-    float kick = (float)(ctx->steps == 0 ? 0.5 * ctx->p.dt : ctx->p.dt);
-    st = walk(ctx, 1, kick, nullptr, false);
-    if (st) return st;
-    st = exchange(ctx);
-    if (st) return st;
+    const int which = ctx->steps == 0 ? 0 : 1;
+    const float kick = (float)(which == 0 ? 0.5 * ctx->p.dt : ctx->p.dt);
+    if (graphs) {
+      cudaGraphExec_t ge;
+      st = step_graph(ctx, which, kick, &ge);
+      if (st) return st;
+      CK(cudaGraphLaunch(ge, ctx->stream));
+      ctx->sort_buf = 0;  // 8 passes: the sorted keys end in buffer 0
+    } else {
+      st = enqueue_step(ctx, kick);
+      if (st) return st;
+    }
     ctx->steps++;
     ctx->tree_valid = false;
   }
@@ -650,6 +706,7 @@ bh_status bh_destroy(bh_ctx *ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto &pp : ctx->pending) { cudaEventDestroy(pp.a); cudaEventDestroy(pp.b); }
   for (auto e : ctx->free_events) cudaEventDestroy(e);
+  drop_graphs(ctx);
   if (ctx->status_ev) cudaEventDestroy(ctx->status_ev);
   if (ctx->hstatus) cudaFreeHost(ctx->hstatus);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -856,6 +913,7 @@ bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *ca
 bh_status bh_set_walk_stats(bh_ctx *ctx, int enable) {
   if (!ctx) return BH_ERR_ARG;
   ctx->walk_stats = enable ? 1 : 0;
+  drop_graphs(ctx);  // the captured steps bake in the walk variant
   if (enable) {
     bh_status st = set_dev(ctx);
     if (st) return st;

@@ -11,7 +11,7 @@
 // All fp32 operations use explicit round-to-nearest intrinsics so nvcc cannot
 // contract them into FMAs: the keys are bit-identical to the oracle's.
 //
-// HBM roofline: K0 reads 16 B/particle; K1 reads 16 B and writes 12 B/particle,
+// HBM roofline: K0 reads 16 B/particle; K1 reads 16 B and writes 8 B/particle,
 // and also builds the 8 digit histograms of the radix sort (one read saved).
 #include <math.h>
 
@@ -143,13 +143,16 @@ __global__ void __launch_bounds__(256) k_keys(const float4 *__restrict__ pos4, i
       float4 p = __ldg(&pos4[i]);
       key = spread3(quantise(p.x, lo0, sc)) << 2 | spread3(quantise(p.y, lo1, sc)) << 1 |
             spread3(quantise(p.z, lo2, sc));
-      keys[i] = key;
-      vals[i] = (uint32_t)i;
+      keys[i] = key;  // the payload (storage id i) is generated by the first sort pass
     }
     unsigned active = __ballot_sync(0xffffffffu, ok);
     if (ok) {
+      // low digits are close to uniform: plain shared atomics; the top digits
+      // of clustered inputs repeat across the warp: warp-aggregated atomics
 #pragma unroll
-      for (int d = 0; d < SORT_PASSES; d++) {
+      for (int d = 0; d < SORT_PASSES - 3; d++) atomicAdd(&sh[d][(uint32_t)(key >> (8 * d)) & 0xffu], 1u);
+#pragma unroll
+      for (int d = SORT_PASSES - 3; d < SORT_PASSES; d++) {
         uint32_t dig = (uint32_t)(key >> (8 * d)) & 0xffu;
         unsigned peers = __match_any_sync(active, dig);
         if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&sh[d][dig], (uint32_t)__popc(peers));

@@ -97,12 +97,11 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_onesweep(const unsigned long lon
   const int64_t wbase = tbase + (int64_t)warp * 32 * SORT_ITEMS;
 
   unsigned long long k[SORT_ITEMS];
-  uint32_t v[SORT_ITEMS], rank[SORT_ITEMS];
+  uint32_t rank[SORT_ITEMS];
 #pragma unroll
   for (int j = 0; j < SORT_ITEMS; j++) {
     int64_t idx = wbase + j * 32 + lane;
-    if (idx < n) { k[j] = kin[idx]; v[j] = vin[idx]; }
-    else { k[j] = 0; v[j] = 0; }
+    k[j] = idx < n ? kin[idx] : 0ull;
   }
   // warp multisplit ranking, stable in (j, lane) order
 #pragma unroll
@@ -167,7 +166,9 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_onesweep(const unsigned long lon
       uint32_t dig = (uint32_t)(k[j] >> shift) & 0xffu;
       uint32_t loc = S.dstart[dig] + S.wcount[warp][dig] + rank[j];
       S.keys[loc] = k[j];
-      S.vals[loc] = v[j];
+      // payload read here (coalesced) rather than held in registers; the first
+      // pass has no payload array: the payload is the storage id itself
+      S.vals[loc] = vin ? vin[idx] : (uint32_t)idx;
     }
   }
   __syncthreads();
@@ -213,7 +214,7 @@ cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *fina
   int src = 0;
   for (int pass = 0; pass < SORT_PASSES; pass++) {
     k_onesweep<<<(unsigned)tiles, SORT_BLOCK, sizeof(SortSmem), s>>>(
-        W.keys[src], W.vals[src], W.keys[src ^ 1], W.vals[src ^ 1], n, 8 * pass, W.sort_hist + pass * SORT_RADIX,
+        W.keys[src], pass == 0 ? nullptr : W.vals[src], W.keys[src ^ 1], W.vals[src ^ 1], n, 8 * pass, W.sort_hist + pass * SORT_RADIX,
         W.sort_status + (size_t)pass * tiles * SORT_RADIX, W.sort_tilectr + pass);
     src ^= 1;
   }
