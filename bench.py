@@ -244,6 +244,18 @@ def ours_arm(args):
     prof = bh.get_profile()
     st1 = bh.get_stats()
     bh.set_profiling(False)
+    # the same K steps without the per-phase events, i.e. through the CUDA-graph
+    # replay of bh_step (one launch per step); reported beside the timed value
+    barrier()
+    torch.cuda.synchronize()
+    eg0, eg1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    bh.step(1)
+    eg0.record(stream)
+    for _ in range(args.steps):
+        bh.step(1)
+    eg1.record(stream)
+    torch.cuda.synchronize()
+    ms_graph = allreduce(eg0.elapsed_time(eg1), dist.ReduceOp.MAX if world > 1 else None) / args.steps
     ms = allreduce(ms_local, dist.ReduceOp.MAX if world > 1 else None)
     inter_local = st1["interactions_cum"] - st0["interactions_cum"]
     # opened-node count (for the flop model) from one untimed stats walk on the
@@ -334,6 +346,7 @@ def ours_arm(args):
             "mac_fallbacks_last_step": st1["mac_fallbacks"],
             "tree_records": st1["n_records"],
             "gpu_launches": int(launches),
+            "ms_per_step_graph_replay": ms_graph,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -97,11 +97,13 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_onesweep(const unsigned long lon
   const int64_t wbase = tbase + (int64_t)warp * 32 * SORT_ITEMS;
 
   unsigned long long k[SORT_ITEMS];
-  uint32_t rank[SORT_ITEMS];
+  uint32_t v[SORT_ITEMS], rank[SORT_ITEMS];
 #pragma unroll
   for (int j = 0; j < SORT_ITEMS; j++) {
     int64_t idx = wbase + j * 32 + lane;
     k[j] = idx < n ? kin[idx] : 0ull;
+    // the first pass has no payload array: the payload is the storage id itself
+    v[j] = vin ? (idx < n ? vin[idx] : 0u) : (uint32_t)idx;
   }
   // warp multisplit ranking, stable in (j, lane) order
 #pragma unroll
@@ -166,9 +168,7 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_onesweep(const unsigned long lon
       uint32_t dig = (uint32_t)(k[j] >> shift) & 0xffu;
       uint32_t loc = S.dstart[dig] + S.wcount[warp][dig] + rank[j];
       S.keys[loc] = k[j];
-      // payload read here (coalesced) rather than held in registers; the first
-      // pass has no payload array: the payload is the storage id itself
-      S.vals[loc] = vin ? vin[idx] : (uint32_t)idx;
+      S.vals[loc] = v[j];
     }
   }
   __syncthreads();
