@@ -76,8 +76,11 @@ typedef struct {
     int64_t node_capacity; /* tree records (internal nodes + particles); 0 = default
                               (n + max(n, min(21 n, 2^22)) + 64, which always fits
                               n <= 199,728 and typical inputs above that)              */
-    int walk_group;     /* lanes sharing one traversal in the force walk: 0 = default (32),
-                           or 1, 2, 4, 8, 16, 32; results are identical for every value     */
+    int walk_group;     /* force-walk variant; every value gives bitwise-identical results:
+                           0 = default (packed fp32, 2 targets per lane, 4 lanes share one
+                           traversal: 8-target groups); 1, 2, 4, 8, 16, 32 = one target per
+                           lane, that many lanes per traversal; 64..70 = packed variants
+                           (64: 32 lanes x 2, 65/69/70: 8/4/2 lanes x 4, 66/67/68: 8/4/2 lanes x 2) */
 } bh_params;
 
 /* Bytes of device workspace the ctx needs for these params (n, world,

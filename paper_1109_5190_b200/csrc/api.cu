@@ -254,8 +254,8 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     return BH_ERR_ARG;
   }
   int g = p->walk_group;
-  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || g == 64 || g == 65)) {
-    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16, 32, 64 or 65");
+  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || (g >= 64 && g <= 70))) {
+    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16, 32 or 64..70");
     return BH_ERR_ARG;
   }
   return BH_OK;

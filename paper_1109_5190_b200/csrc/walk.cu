@@ -603,26 +603,48 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   unsigned grid = (unsigned)((a.n_targets + 255) / 256);
-  if (!a.stats && (a.group == 0 || a.group == 64 || a.group == 65)) {
+  if (!a.stats && (a.group == 0 || a.group >= 64)) {
     // production path: packed fp32 pairs of targets per lane
-    //   0 : 16 lanes x 2 targets (32-target groups)   [default]
+    //   0 : 4 lanes x 2 targets (8-target groups)   [default]
     //   64: 32 lanes x 2 targets (64-target groups)
-    //   65: 8 lanes x 4 targets (32-target groups)
+    //   65 / 69 / 70: 8 / 4 / 2 lanes x 4 targets
+    //   66 / 67 / 68: 8 / 4 / 2 lanes x 2 targets
     const bool cont = a.need_cont;
-    if (a.group == 65) {
+    if (a.group >= 66 && a.group <= 68) {  // 8 / 4 / 2 lanes x 2 targets (16-, 8-, 4-target groups)
+      const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
+      P.n_chunks = grid2;
+      if (a.group == 66) {
+        if (cont) k_walk2<8, 1, true><<<grid2, 256, 0, s>>>(P);
+        else k_walk2<8, 1, false><<<grid2, 256, 0, s>>>(P);
+      } else if (a.group == 67) {
+        if (cont) k_walk2<4, 1, true><<<grid2, 256, 0, s>>>(P);
+        else k_walk2<4, 1, false><<<grid2, 256, 0, s>>>(P);
+      } else {
+        if (cont) k_walk2<2, 1, true><<<grid2, 256, 0, s>>>(P);
+        else k_walk2<2, 1, false><<<grid2, 256, 0, s>>>(P);
+      }
+    } else if (a.group == 65 || a.group == 69 || a.group == 70) {  // 4 targets per lane
       const unsigned g4 = (unsigned)((a.n_targets + 1023) / 1024);
       P.n_chunks = g4;
-      if (cont) k_walk2<8, 2, true><<<g4, 256, 0, s>>>(P);
-      else k_walk2<8, 2, false><<<g4, 256, 0, s>>>(P);
+      if (a.group == 65) {
+        if (cont) k_walk2<8, 2, true><<<g4, 256, 0, s>>>(P);
+        else k_walk2<8, 2, false><<<g4, 256, 0, s>>>(P);
+      } else if (a.group == 69) {
+        if (cont) k_walk2<4, 2, true><<<g4, 256, 0, s>>>(P);
+        else k_walk2<4, 2, false><<<g4, 256, 0, s>>>(P);
+      } else {
+        if (cont) k_walk2<2, 2, true><<<g4, 256, 0, s>>>(P);
+        else k_walk2<2, 2, false><<<g4, 256, 0, s>>>(P);
+      }
     } else {
       const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
       P.n_chunks = grid2;
       if (a.group == 64) {
         if (cont) k_walk2<32, 1, true><<<grid2, 256, 0, s>>>(P);
         else k_walk2<32, 1, false><<<grid2, 256, 0, s>>>(P);
-      } else {
-        if (cont) k_walk2<16, 1, true><<<grid2, 256, 0, s>>>(P);
-        else k_walk2<16, 1, false><<<grid2, 256, 0, s>>>(P);
+      } else {  // default: 4 lanes x 2 targets = 8-target groups (fastest on cfg3-cfg5)
+        if (cont) k_walk2<4, 1, true><<<grid2, 256, 0, s>>>(P);
+        else k_walk2<4, 1, false><<<grid2, 256, 0, s>>>(P);
       }
     }
   } else {

@@ -211,7 +211,7 @@ def test_errors(BH):
     assert e.value.code == -3
 
 
-@pytest.mark.parametrize("group", [1, 4, 16, 32, 64, 65])
+@pytest.mark.parametrize("group", [1, 4, 16, 32, 64, 65, 66, 67, 68, 69, 70])
 def test_walk_group_invariance(BH, group):
     """The traversal-sharing group size changes nothing: bitwise equal forces."""
     m, p, v = bhgen.generate("cfg2", n=20000)
