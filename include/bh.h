@@ -80,7 +80,10 @@ typedef struct {
                            0 = default (packed fp32, 2 targets per lane, 4 lanes share one
                            traversal: 8-target groups); 1, 2, 4, 8, 16, 32 = one target per
                            lane, that many lanes per traversal; 64..70 = packed variants
-                           (64: 32 lanes x 2, 65/69/70: 8/4/2 lanes x 4, 66/67/68: 8/4/2 lanes x 2) */
+                           (64: 32 lanes x 2, 65/69/70: 8/4/2 lanes x 4, 66/67/68: 8/4/2 lanes x 2);
+                           80..85 = persistent lane groups (80: 1 x 4, 81: 1 x 2, 82: 2 x 4,
+                           83: 2 x 2, 84: 4 x 2, 85: 4 x 4 lanes x targets), 90..95 = the same
+                           groups without persistence (one group per slot)                 */
 } bh_params;
 
 /* Bytes of device workspace the ctx needs for these params (n, world,

@@ -254,8 +254,9 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     return BH_ERR_ARG;
   }
   int g = p->walk_group;
-  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || (g >= 64 && g <= 70))) {
-    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16, 32 or 64..70");
+  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || (g >= 64 && g <= 70) ||
+        (g >= 80 && g <= 85) || (g >= 90 && g <= 95))) {
+    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16, 32, 64..70, 80..85 or 90..95");
     return BH_ERR_ARG;
   }
   return BH_OK;
@@ -384,7 +385,7 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.own_lo = (uint32_t)ctx->own_lo;
   a.acc_out = mode == 0 ? acc_out : nullptr;
   a.user_order = user_order ? 1 : 0;
-  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 5 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 6 * sizeof(unsigned long long), s));
   if (ctx->p.world > 1) {
     CK(launch_own_targets(ctx->W, n, ctx->sort_buf, (uint32_t)ctx->own_lo, (uint32_t)ctx->own_hi, s));
     a.use_targets = 1;

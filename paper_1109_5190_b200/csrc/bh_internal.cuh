@@ -57,6 +57,7 @@ struct DevStatus {
   unsigned long long opens;          // last walk: MAC tests that opened a node (incl. self leaf)
   unsigned long long iters;          // last walk: group-loop iterations summed over lanes
   unsigned long long n_redo;         // last walk: targets re-walked with the exact fp64 MAC
+  unsigned long long walk_next;      // last walk: next target group of the persistent lane walk
   uint32_t sm_next[256];             // walk: next chunk of each SM's segment (zeroed per walk)
   unsigned long long interactions_cum;  // since create / set_state
   unsigned long long opens_cum;

@@ -436,6 +436,239 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
   }
 }
 
+// ---------------------------------------------------------------- k_walk_lane
+// Variant family (walk_group 80..85, 90..95): groups of GL lanes x TPL = 2 NP
+// targets with a leaner MAC (mac_pair: predicates in one asm block, 7 ALU ops
+// per target instead of 9-10) and one LDG.256 per record visit; the per-target
+// semantics and the fp32 operation sequence are exactly those of k_walk /
+// k_walk2 (bitwise-identical results).  80..85 are persistent (a lane group
+// that finishes takes the next group from per-SM Morton segments, so no group
+// idles behind a slower one in its warp); 90..95 give every group slot one
+// group, like k_walk2.
+// Measured on cfg4 (profiles/r1_walk_variants.md): none beats
+// k_walk2<4,1> (49.3 ms).  The loop is bound by L1 register writeback (32 B per
+// lane per visit: 64-75 % of the LSU writeback peak) and by load latency,
+// not by issue: cutting instructions by 8-12 % (83, 93) gains nothing, 4
+// targets per lane (80, 82, 92) halves the writeback but needs 80 registers
+// (24 warps/SM) and loses L1 hits (34-45 % with persistent scheduling, whose
+// warps are at unrelated depths of their walks, vs 86 % for k_walk2's
+// phase-aligned blocks).  Kept as measured alternatives.
+__device__ __forceinline__ void ld_rec(const Rec *p, float4 &cm, uint4 &au) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(cm.x), "=f"(cm.y), "=f"(cm.z), "=f"(cm.w), "=r"(au.x), "=r"(au.y), "=r"(au.z), "=r"(au.w)
+               : "l"(p));
+}
+
+// One target's MAC decision at record cc, as bit masks (few live predicates):
+//   act = cc >= res (and, with CONT, the record does not contain the target)
+//   acc = act & d2 > T_acc      -> interact (f kept), cnt += 1, res = skip
+//   amb = act & !acc & d2 >= T_rej -> inconclusive: res = ~0 (re-walked exactly)
+//   opn |= act & d2 < T_rej     -> the lane descends
+// Identical decisions to k_walk / k_walk2.
+__device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, float tacc, float trej, uint32_t skip,
+                                         uint32_t &resA, uint32_t &resB, uint32_t &cntA, uint32_t &cntB,
+                                         uint32_t &opn, float &fA, float &fB) {
+  asm("{\n\t.reg .pred pa, pc, pq, pb, pd, pr, po;\n\t"
+      "setp.ge.u32 pa, %9, %0;\n\t"                 // act A
+      "setp.gt.and.f32 pc, %10, %12, pa;\n\t"       // acc A
+      "setp.ge.and.f32 pq, %10, %13, pa;\n\t"       // acc-or-amb A
+      "setp.ge.u32 pb, %9, %1;\n\t"                 // act B
+      "setp.gt.and.f32 pd, %11, %12, pb;\n\t"       // acc B
+      "setp.ge.and.f32 pr, %11, %13, pb;\n\t"       // acc-or-amb B
+      "@pc add.u32 %2, %2, 1;\n\t"
+      "@pd add.u32 %3, %3, 1;\n\t"
+      "@pq selp.b32 %0, %14, 0xffffffff, pc;\n\t"   // acc: skip; amb: ~0 (re-walk)
+      "@pr selp.b32 %1, %14, 0xffffffff, pd;\n\t"
+      "@!pc mov.b32 %5, 0f00000000;\n\t"
+      "@!pd mov.b32 %6, 0f00000000;\n\t"
+      "not.pred pq, pq;\n\t"
+      "not.pred pr, pr;\n\t"
+      "and.pred pa, pa, pq;\n\t"
+      "and.pred pb, pb, pr;\n\t"
+      "or.pred po, pa, pb;\n\t"
+      "@po mov.b32 %4, 1;\n\t}"
+      : "+r"(resA), "+r"(resB), "+r"(cntA), "+r"(cntB), "+r"(opn), "+f"(fA), "+f"(fB)
+      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip));
+}
+
+template <int GL, int NP, bool CONT, bool PERSIST>
+__global__ void __launch_bounds__(256, (NP == 1 || !PERSIST) ? 4 : 3) k_walk_lane(const WalkParams P) {
+  constexpr int TPL = 2 * NP;       // targets per lane
+  constexpr int GT = GL * TPL;      // targets per group
+  const uint32_t full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % GL;         // lane within the group
+  const int glead = lane & ~(GL - 1);
+  const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << glead);
+  if (P.st->err & ERR_NODE_OVERFLOW) return;
+  const uint32_t Wn = P.st->n_records;
+  const int64_t ngroups = (P.n_targets + GT - 1) / GT;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t Li[TPL], res[TPL], cnt[TPL];
+  float ax[TPL], ay[TPL], az[TPL];
+  F2 X[NP], Y[NP], Z[NP];
+#pragma unroll
+  for (int k = 0; k < TPL; k++) {
+    Li[k] = 0;
+    res[k] = 0xffffffffu;
+    cnt[k] = 0;
+    ax[k] = ay[k] = az[k] = 0.f;
+  }
+#pragma unroll
+  for (int j = 0; j < NP; j++) X[j] = Y[j] = Z[j] = pk2(0.f, 0.f);
+  const F2 E2 = pk2(P.eps2, P.eps2);
+  const Rec *__restrict__ rec = P.rec;
+  uint32_t gm = gmask;
+  asm volatile("" : "+r"(gm));      // a plain register: the group test is one LOP3
+  int64_t g = -1;                   // current group (-1: none yet)
+  bool parked = false;              // no groups left for this lane's group
+  const int nseg = P.num_sms < 256 ? P.num_sms : 256;
+  int seg, hops = 0;                // ticket segment (warp-uniform), segments exhausted
+  bool first_done = false;
+  asm("mov.u32 %0, %%smid;" : "=r"(seg));
+  seg %= nseg;
+  uint32_t c = Wn;                  // cursor (group-uniform); Wn = the sentinel record
+  unsigned long long wc = 0;
+  for (;;) {
+    const bool need = (c >= Wn) & !parked;   // group-uniform
+    if (__any_sync(full, need)) {
+      if (need && g >= 0) {  // write the finished group's results
+#pragma unroll
+        for (int k = 0; k < TPL; k++) {
+          const int64_t t = g * GT + gl * TPL + k;
+          if (t >= P.n_targets) continue;
+          if (!CONT) cnt[k] -= 1u;  // own record: "accepted", zero contribution
+          if (res[k] == 0xffffffffu) {
+            P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)t;
+          } else {
+            wc += cnt[k];
+            finish(P, load_target(P, t), (double)ax[k], (double)ay[k], (double)az[k], cnt[k]);
+          }
+        }
+      }
+      // one ticket per group that needs work.  The groups are split into one
+      // contiguous Morton segment per SM; a warp takes tickets from its SM's
+      // segment first (the warps resident on an SM then walk neighbouring
+      // regions and share L1) and steals from the following segments after.
+      int64_t mine = INT64_MAX;
+      if (!PERSIST) {  // one group per group slot of the grid, no refill
+        if (g < 0 && !first_done) mine = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GL;
+        first_done = true;
+      } else {
+        const uint32_t m = __ballot_sync(full, need & (gl == 0));
+        const int rank = __popc(m & lt);
+        int left = __popc(m);
+        int assigned = 0;
+        while (left > 0 && hops < nseg) {
+          const int64_t lo = ngroups * seg / nseg, hi = ngroups * (seg + 1) / nseg;
+          uint32_t b = 0;
+          if (lane == 0) b = atomicAdd(&P.st->sm_next[seg], (uint32_t)left);
+          b = __shfl_sync(full, b, 0);
+          const int64_t avail = hi - lo - (int64_t)b;
+          const int take = avail <= 0 ? 0 : (avail < left ? (int)avail : left);
+          if (rank >= assigned && rank < assigned + take) mine = lo + b + (rank - assigned);
+          assigned += take;
+          left -= take;
+          if (left > 0) {
+            seg = seg + 1 == nseg ? 0 : seg + 1;
+            hops++;
+          }
+        }
+      }
+      const int64_t gnew = GL == 1 ? mine : __shfl_sync(full, mine, glead);
+      if (need) {
+        g = gnew;
+        if (g >= ngroups) {
+          parked = true;
+          g = -1;
+        } else {
+#pragma unroll
+          for (int k = 0; k < TPL; k++) {
+            const int64_t t = g * GT + gl * TPL + k;
+            float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t < P.n_targets) {
+              const Target T = load_target(P, t);
+              me = T.me;
+              Li[k] = T.Li;
+              res[k] = 0u;
+            } else {
+              res[k] = 0xffffffffu;
+            }
+            cnt[k] = 0;
+            ax[k] = ay[k] = az[k] = 0.f;
+            if (k & 1) {
+              float lo, hi;
+              up2(X[k >> 1], lo, hi);
+              X[k >> 1] = pk2(lo, me.x);
+              up2(Y[k >> 1], lo, hi);
+              Y[k >> 1] = pk2(lo, me.y);
+              up2(Z[k >> 1], lo, hi);
+              Z[k >> 1] = pk2(lo, me.z);
+            } else {
+              X[k >> 1] = pk2(me.x, 0.f);
+              Y[k >> 1] = pk2(me.y, 0.f);
+              Z[k >> 1] = pk2(me.z, 0.f);
+            }
+          }
+          c = 0;
+        }
+      }
+      if (__all_sync(full, parked)) break;
+    }
+#pragma unroll 2
+    for (int u = 0; u < 2; u++) {
+      const uint32_t cc = c;
+      float4 cm;
+      uint4 au;
+      ld_rec(rec + cc, cm, au);
+      const uint32_t skip = au.z;
+      const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
+      uint32_t opn = 0u;
+#pragma unroll
+      for (int j = 0; j < NP; j++) {
+        const int a = 2 * j, b = 2 * j + 1;
+        const F2 DX = sub2(pk2(cm.x, cm.x), X[j]), DY = sub2(pk2(cm.y, cm.y), Y[j]),
+                 DZ = sub2(pk2(cm.z, cm.z), Z[j]);
+        const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
+        float d2A, d2B;
+        up2(D2, d2A, d2B);
+        float r2A, r2B;
+        up2(add2(D2, E2), r2A, r2B);
+        const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
+        float fA, fB;
+        up2(mul2(mul2(pk2(cm.w, cm.w), mul2(INV, INV)), INV), fA, fB);
+        if (CONT) {
+          // a record containing the target is opened, never accepted (NaN
+          // distance: every comparison is false)
+          const bool cA = (cc <= Li[a]) & (skip > Li[a]), cB = (cc <= Li[b]) & (skip > Li[b]);
+          const float qnan = __int_as_float(0x7fffffff);
+          mac_pair(cc, cA ? qnan : d2A, cB ? qnan : d2B, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA,
+                   fB);
+        } else {
+          mac_pair(cc, d2A, d2B, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA, fB);
+        }
+        const F2 FF = pk2(fA, fB);
+        asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+            : "+f"(ax[a]), "+f"(ax[b]) : "l"(FF.v), "l"(DX.v));
+        asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+            : "+f"(ay[a]), "+f"(ay[b]) : "l"(FF.v), "l"(DY.v));
+        asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+            : "+f"(az[a]), "+f"(az[b]) : "l"(FF.v), "l"(DZ.v));
+      }
+      // the group descends if any of its targets opens; a group at the sentinel
+      // (walk over, or parked: every res = ~0) stays there
+      const bool go = GL == 1 ? opn != 0u : (__ballot_sync(full, opn != 0u) & gm) != 0u;
+      c = min(go ? cc + 1u : skip, Wn);
+    }
+  }
+  for (int o = 16; o; o >>= 1) wc += __shfl_xor_sync(full, wc, o);
+  if (lane == 0 && wc) {
+    atomicAdd(&P.st->interactions, wc);
+    atomicAdd(&P.st->interactions_cum, wc);
+  }
+}
+
 // Exact walk of the queued targets.  One WARP per target: the node set a target
 // interacts with does not depend on the visiting order, so the warp expands the
 // target's frontier 32 nodes at a time from a LIFO stack in shared memory
@@ -598,12 +831,63 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.own_lo = a.own_lo;
   P.sm_local = a.sm_local;
   P.num_sms = a.num_sms > 0 ? a.num_sms : 148;
-  if (P.sm_local) {
+  if (P.sm_local || (!a.stats && a.group >= 80 && a.group <= 95)) {
     cudaError_t e = cudaMemsetAsync(W.status->sm_next, 0, sizeof(W.status->sm_next), s);
     if (e != cudaSuccess) return e;
   }
   unsigned grid = (unsigned)((a.n_targets + 255) / 256);
-  if (!a.stats && (a.group == 0 || a.group >= 64)) {
+  if (!a.stats && a.group >= 80 && a.group <= 95) {
+    // group walk (k_walk_lane): lanes per group x targets per lane
+    //   80: 1 x 4   81: 1 x 2   82: 2 x 4   83: 2 x 2   84: 4 x 2   85: 4 x 4
+    //   (persistent, SM-local tickets); +10: the same, one group per slot
+    const bool cont = a.need_cont;
+    const bool persist = a.group < 90;
+    const int code = persist ? a.group : a.group - 10;
+    cudaError_t e = cudaSuccess;
+    int nb = 0, tpg = 4;
+#define BH_LANE_CASE(code, GLv, NPv)                                                                 \
+  case code:                                                                                          \
+    tpg = GLv * 2 * NPv;                                                                              \
+    e = cont ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_walk_lane<GLv, NPv, true, true>, 256, 0) \
+             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_walk_lane<GLv, NPv, false, true>, 256, 0); \
+    break;
+    switch (code) {
+      BH_LANE_CASE(80, 1, 2)
+      BH_LANE_CASE(81, 1, 1)
+      BH_LANE_CASE(82, 2, 2)
+      BH_LANE_CASE(83, 2, 1)
+      BH_LANE_CASE(84, 4, 1)
+      BH_LANE_CASE(85, 4, 2)
+    }
+#undef BH_LANE_CASE
+    if (e != cudaSuccess) return e;
+    if (nb < 1) nb = 1;
+    const int64_t ngroups = (a.n_targets + tpg - 1) / tpg;
+    const int lanes_per_group = code == 80 || code == 81 ? 1 : (code <= 83 ? 2 : 4);
+    int64_t want = (ngroups * lanes_per_group + 255) / 256;  // no more threads than groups need
+    int64_t gl = (int64_t)P.num_sms * nb;
+    if (want < gl || !persist) gl = want;
+    const unsigned gridl = (unsigned)(gl < 1 ? 1 : gl);
+#define BH_LANE_LAUNCH(code, GLv, NPv)                                   \
+  case code:                                                             \
+    if (persist) {                                                       \
+      if (cont) k_walk_lane<GLv, NPv, true, true><<<gridl, 256, 0, s>>>(P);  \
+      else k_walk_lane<GLv, NPv, false, true><<<gridl, 256, 0, s>>>(P);      \
+    } else {                                                             \
+      if (cont) k_walk_lane<GLv, NPv, true, false><<<gridl, 256, 0, s>>>(P); \
+      else k_walk_lane<GLv, NPv, false, false><<<gridl, 256, 0, s>>>(P);     \
+    }                                                                    \
+    break;
+    switch (code) {
+      BH_LANE_LAUNCH(80, 1, 2)
+      BH_LANE_LAUNCH(81, 1, 1)
+      BH_LANE_LAUNCH(82, 2, 2)
+      BH_LANE_LAUNCH(83, 2, 1)
+      BH_LANE_LAUNCH(84, 4, 1)
+      BH_LANE_LAUNCH(85, 4, 2)
+    }
+#undef BH_LANE_LAUNCH
+  } else if (!a.stats && (a.group == 0 || a.group >= 64)) {
     // production path: packed fp32 pairs of targets per lane
     //   0 : 4 lanes x 2 targets (8-target groups)   [default]
     //   64: 32 lanes x 2 targets (64-target groups)

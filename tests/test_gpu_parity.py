@@ -211,11 +211,13 @@ def test_errors(BH):
     assert e.value.code == -3
 
 
-@pytest.mark.parametrize("group", [1, 4, 16, 32, 64, 65, 66, 67, 68, 69, 70])
-def test_walk_group_invariance(BH, group):
-    """The traversal-sharing group size changes nothing: bitwise equal forces."""
-    m, p, v = bhgen.generate("cfg2", n=20000)
-    prm = bhgen.params("cfg2")
+@pytest.mark.parametrize("cfg,group", [("cfg2", g) for g in (1, 4, 16, 32, 64, 65, 66, 67, 68, 69, 70, 80, 81, 82, 83, 84, 85, 92, 93, 94)]
+                         + [("cfg3", g) for g in (1, 32, 67, 80, 81, 82, 83, 84, 85, 90, 92, 93, 94, 95)])
+def test_walk_group_invariance(BH, cfg, group):
+    """The traversal-sharing group size changes nothing: bitwise equal forces
+    (cfg2: theta = 0.5, containment test elided; cfg3: theta = 0.7, kept)."""
+    m, p, v = bhgen.generate(cfg, n=20000)
+    prm = bhgen.params(cfg)
     a = BH(m, p, v, **prm)
     a.build_tree()
     ref = a.compute_forces()
