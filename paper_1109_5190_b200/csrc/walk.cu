@@ -288,13 +288,51 @@ __device__ __forceinline__ void fma2_acc(F2 &acc, F2 a, F2 b) {  // acc = a * b 
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.v) : "l"(a.v), "l"(b.v));
 }
 
+__device__ __forceinline__ void ld_rec(const Rec *p, float4 &cm, uint4 &au) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(cm.x), "=f"(cm.y), "=f"(cm.z), "=f"(cm.w), "=r"(au.x), "=r"(au.y), "=r"(au.z), "=r"(au.w)
+               : "l"(p));
+}
+
+// One target's MAC decision at record cc, as bit masks (few live predicates):
+//   act = cc >= res (and, with CONT, the record does not contain the target)
+//   acc = act & d2 > T_acc      -> interact (f kept), cnt += 1, res = skip
+//   amb = act & !acc & d2 >= T_rej -> inconclusive: res = ~0 (re-walked exactly)
+//   opn |= act & d2 < T_rej     -> the lane descends
+// Identical decisions to k_walk / k_walk2.
+__device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, float tacc, float trej, uint32_t skip,
+                                         uint32_t &resA, uint32_t &resB, uint32_t &cntA, uint32_t &cntB,
+                                         uint32_t &opn, float &fA, float &fB) {
+  asm("{\n\t.reg .pred pa, pc, pq, pb, pd, pr, po;\n\t"
+      "setp.ge.u32 pa, %9, %0;\n\t"                 // act A
+      "setp.gt.and.f32 pc, %10, %12, pa;\n\t"       // acc A
+      "setp.ge.and.f32 pq, %10, %13, pa;\n\t"       // acc-or-amb A
+      "setp.ge.u32 pb, %9, %1;\n\t"                 // act B
+      "setp.gt.and.f32 pd, %11, %12, pb;\n\t"       // acc B
+      "setp.ge.and.f32 pr, %11, %13, pb;\n\t"       // acc-or-amb B
+      "@pc add.u32 %2, %2, 1;\n\t"
+      "@pd add.u32 %3, %3, 1;\n\t"
+      "@pq selp.b32 %0, %14, 0xffffffff, pc;\n\t"   // acc: skip; amb: ~0 (re-walk)
+      "@pr selp.b32 %1, %14, 0xffffffff, pd;\n\t"
+      "@!pc mov.b32 %5, 0f00000000;\n\t"
+      "@!pd mov.b32 %6, 0f00000000;\n\t"
+      "not.pred pq, pq;\n\t"
+      "not.pred pr, pr;\n\t"
+      "and.pred pa, pa, pq;\n\t"
+      "and.pred pb, pb, pr;\n\t"
+      "or.pred po, pa, pb;\n\t"
+      "@po mov.b32 %4, 1;\n\t}"
+      : "+r"(resA), "+r"(resB), "+r"(cntA), "+r"(cntB), "+r"(opn), "+f"(fA), "+f"(fB)
+      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip));
+}
+
 #ifndef BH_WALK2_MINB
 #define BH_WALK2_MINB 5
 #endif
 // NP pairs of targets per lane (2 NP targets), GL lanes per group: a group of
 // 2 NP GL Morton-consecutive targets shares one traversal.
 template <int GL, int NP, bool CONT>
-__global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P) {
+__global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(const WalkParams P) {
   constexpr int TPL = 2 * NP;  // targets per lane
   const uint32_t full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -359,6 +397,7 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
   const F2 E2 = pk2(P.eps2, P.eps2);
   const bool gvalid = (__ballot_sync(full, anyv) & gmask) != 0u;
   const Rec *__restrict__ rec = P.rec;
+  asm volatile("" : "+l"(rec));  // base in a register (no per-iteration constant reload)
   uint32_t gmask2 = gmask;
   asm volatile("" : "+r"(gmask2));  // a plain register: the group test is one LOP3
   uint32_t c = gvalid ? 0u : Wn;
@@ -366,11 +405,12 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
   // skip = Wn: nothing is accepted or queued there) until the warp is done
   if (__any_sync(full, c < Wn)) for (;;) {
     const uint32_t cc = c;
-    const float4 cm = __ldg(&rec[cc].cm);
-    const uint4 au = __ldg(&rec[cc].aux);
+    float4 cm;
+    uint4 au;
+    ld_rec(rec + cc, cm, au);
     const uint32_t skip = au.z;
     const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
-    bool opn = false;
+    uint32_t opn = 0u;
 #pragma unroll
     for (int j = 0; j < NP; j++) {
       const int a = 2 * j, b = 2 * j + 1;
@@ -379,22 +419,26 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
       const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
       float d2A, d2B;
       up2(D2, d2A, d2B);
-      // per-target MAC (identical decisions to k_walk)
-      const bool actA = cc >= res[a], actB = cc >= res[b];
-      const bool okA = CONT ? actA & !((cc <= Li[a]) & (skip > Li[a])) : actA;
-      const bool okB = CONT ? actB & !((cc <= Li[b]) & (skip > Li[b])) : actB;
-      const bool accA = okA & (d2A > tacc), accB = okB & (d2B > tacc);
-      // inconclusive fp32 test: the target drops out (resume = ~0) and is
-      // re-walked with the exact fp64 test by k_walk_exact
-      const bool ambA = okA & !accA & (d2A >= trej), ambB = okB & !accB & (d2B >= trej);
-      opn |= (actA & !accA & !ambA) | (actB & !accB & !ambB);
-      // interaction for both targets of the pair, branch-free
+      // interaction for both targets of the pair, branch-free (f zeroed below
+      // for a target that does not accept the record)
       float r2A, r2B;
       up2(add2(D2, E2), r2A, r2B);
       const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
       float fA, fB;
       up2(mul2(mul2(pk2(cm.w, cm.w), mul2(INV, INV)), INV), fA, fB);
-      const F2 FF = pk2(accA ? fA : 0.0f, accB ? fB : 0.0f);
+      // per-target MAC (identical decisions to k_walk); an inconclusive fp32
+      // test drops the target out (resume = ~0): k_walk_exact re-walks it
+      if (CONT) {
+        // a record containing the target is opened, never accepted (NaN
+        // distance: every comparison is false)
+        const bool cA = (cc <= Li[a]) & (skip > Li[a]), cB = (cc <= Li[b]) & (skip > Li[b]);
+        const float qnan = __int_as_float(0x7fffffff);
+        mac_pair(cc, cA ? qnan : d2A, cB ? qnan : d2B, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA,
+                 fB);
+      } else {
+        mac_pair(cc, d2A, d2B, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA, fB);
+      }
+      const F2 FF = pk2(fA, fB);
       // packed accumulate on (a, b) register pairs (this form avoids ptxas moves)
       asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
           : "+f"(ax[a]), "+f"(ax[b]) : "l"(FF.v), "l"(DX.v));
@@ -402,15 +446,11 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
           : "+f"(ay[a]), "+f"(ay[b]) : "l"(FF.v), "l"(DY.v));
       asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
           : "+f"(az[a]), "+f"(az[b]) : "l"(FF.v), "l"(DZ.v));
-      asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cnt[a]) : "r"((uint32_t)accA));
-      asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cnt[b]) : "r"((uint32_t)accB));
-      res[a] = accA ? skip : (ambA ? 0xffffffffu : res[a]);
-      res[b] = accB ? skip : (ambB ? 0xffffffffu : res[b]);
     }
     if (GL == 32) {
-      c = __any_sync(full, opn) ? cc + 1u : skip;
+      c = __any_sync(full, opn != 0u) ? cc + 1u : skip;
     } else {
-      const uint32_t nxt = (__ballot_sync(full, opn) & gmask2) ? cc + 1u : skip;
+      const uint32_t nxt = (__ballot_sync(full, opn != 0u) & gmask2) ? cc + 1u : skip;
       c = min(nxt, Wn);
     }
     if (!__any_sync(full, c < Wn)) break;
@@ -453,44 +493,6 @@ __global__ void __launch_bounds__(256, BH_WALK2_MINB) k_walk2(const WalkParams P
 // (24 warps/SM) and loses L1 hits (34-45 % with persistent scheduling, whose
 // warps are at unrelated depths of their walks, vs 86 % for k_walk2's
 // phase-aligned blocks).  Kept as measured alternatives.
-__device__ __forceinline__ void ld_rec(const Rec *p, float4 &cm, uint4 &au) {
-  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=f"(cm.x), "=f"(cm.y), "=f"(cm.z), "=f"(cm.w), "=r"(au.x), "=r"(au.y), "=r"(au.z), "=r"(au.w)
-               : "l"(p));
-}
-
-// One target's MAC decision at record cc, as bit masks (few live predicates):
-//   act = cc >= res (and, with CONT, the record does not contain the target)
-//   acc = act & d2 > T_acc      -> interact (f kept), cnt += 1, res = skip
-//   amb = act & !acc & d2 >= T_rej -> inconclusive: res = ~0 (re-walked exactly)
-//   opn |= act & d2 < T_rej     -> the lane descends
-// Identical decisions to k_walk / k_walk2.
-__device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, float tacc, float trej, uint32_t skip,
-                                         uint32_t &resA, uint32_t &resB, uint32_t &cntA, uint32_t &cntB,
-                                         uint32_t &opn, float &fA, float &fB) {
-  asm("{\n\t.reg .pred pa, pc, pq, pb, pd, pr, po;\n\t"
-      "setp.ge.u32 pa, %9, %0;\n\t"                 // act A
-      "setp.gt.and.f32 pc, %10, %12, pa;\n\t"       // acc A
-      "setp.ge.and.f32 pq, %10, %13, pa;\n\t"       // acc-or-amb A
-      "setp.ge.u32 pb, %9, %1;\n\t"                 // act B
-      "setp.gt.and.f32 pd, %11, %12, pb;\n\t"       // acc B
-      "setp.ge.and.f32 pr, %11, %13, pb;\n\t"       // acc-or-amb B
-      "@pc add.u32 %2, %2, 1;\n\t"
-      "@pd add.u32 %3, %3, 1;\n\t"
-      "@pq selp.b32 %0, %14, 0xffffffff, pc;\n\t"   // acc: skip; amb: ~0 (re-walk)
-      "@pr selp.b32 %1, %14, 0xffffffff, pd;\n\t"
-      "@!pc mov.b32 %5, 0f00000000;\n\t"
-      "@!pd mov.b32 %6, 0f00000000;\n\t"
-      "not.pred pq, pq;\n\t"
-      "not.pred pr, pr;\n\t"
-      "and.pred pa, pa, pq;\n\t"
-      "and.pred pb, pb, pr;\n\t"
-      "or.pred po, pa, pb;\n\t"
-      "@po mov.b32 %4, 1;\n\t}"
-      : "+r"(resA), "+r"(resB), "+r"(cntA), "+r"(cntB), "+r"(opn), "+f"(fA), "+f"(fB)
-      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip));
-}
-
 template <int GL, int NP, bool CONT, bool PERSIST>
 __global__ void __launch_bounds__(256, (NP == 1 || !PERSIST) ? 4 : 3) k_walk_lane(const WalkParams P) {
   constexpr int TPL = 2 * NP;       // targets per lane
@@ -519,6 +521,7 @@ __global__ void __launch_bounds__(256, (NP == 1 || !PERSIST) ? 4 : 3) k_walk_lan
   for (int j = 0; j < NP; j++) X[j] = Y[j] = Z[j] = pk2(0.f, 0.f);
   const F2 E2 = pk2(P.eps2, P.eps2);
   const Rec *__restrict__ rec = P.rec;
+  asm volatile("" : "+l"(rec));  // base in a register (no per-iteration constant reload)
   uint32_t gm = gmask;
   asm volatile("" : "+r"(gm));      // a plain register: the group test is one LOP3
   int64_t g = -1;                   // current group (-1: none yet)
