@@ -87,7 +87,10 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
   if (worst > ((int64_t)1 << 22)) worst = (int64_t)1 << 22;
   if (worst > def_int) def_int = worst;
   L.cap_rec = node_capacity > 0 ? node_capacity : n + def_int + 64;
+  if (L.cap_rec > BH_MAX_RECORDS) L.cap_rec = BH_MAX_RECORDS;  // record indices stay below the walk's drop flag
   L.cap_int = L.cap_rec - n;
+  L.cap_resume = n / 8 > 65536 ? n / 8 : 65536;
+  if (L.cap_resume > n) L.cap_resume = n;
   L.n_own_max = (n + world - 1) / world + 1;
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
@@ -109,7 +112,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
       sizeof(uint32_t) * (SORT_PASSES * SORT_RADIX + 8 + (size_t)SORT_PASSES * L.sort_tiles * SORT_RADIX),  // 14
       sizeof(float) * 8 * BBOX_BLOCKS,         // 15 bbox partials
       (size_t)L.cap_rec * 32,                  // 16 rec (cm + aux)
-      0,                                       // 17 (unused)
+      (size_t)L.cap_resume * sizeof(ResumeState),  // 17 walk resume states
       (size_t)L.cap_rec * 4,                   // 18 rec_first
       (size_t)L.cap_rec * 32,                  // 19 rec_mom
       (size_t)L.cap_int * 4,                   // 20 lvl_list
@@ -145,6 +148,8 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.sort_status = W.sort_tilectr + 8;
   W.bbox_part = (float *)(b + L.off[15]);
   W.rec = (Rec *)(b + L.off[16]);
+  W.resume = (ResumeState *)(b + L.off[17]);
+  W.cap_resume = L.cap_resume;
   W.rec_first = (uint32_t *)(b + L.off[18]);
   W.rec_mom = (double4 *)(b + L.off[19]);
   W.lvl_list = (uint32_t *)(b + L.off[20]);
@@ -249,8 +254,8 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     snprintf(err, errn, "need 0 <= rank < world <= n");
     return BH_ERR_ARG;
   }
-  if (p->node_capacity != 0 && p->node_capacity < p->n + 1) {
-    snprintf(err, errn, "node_capacity must be 0 or >= n + 1");
+  if (p->node_capacity != 0 && (p->node_capacity < p->n + 1 || p->node_capacity > BH_MAX_RECORDS)) {
+    snprintf(err, errn, "node_capacity must be 0 or in [n + 1, 2^31 - 2]");
     return BH_ERR_ARG;
   }
   int g = p->walk_group;

@@ -80,6 +80,21 @@ struct __align__(32) Rec {
   uint4 aux;
 };
 
+// record indices (and the sentinel) stay below 2^31: the walk marks a target
+// whose fp32 MAC test was inconclusive with resume = BH_DROP | record
+#define BH_MAX_RECORDS 0x7ffffffeLL
+#define BH_DROP 0x80000000u
+
+// state of a target that dropped out of the fast walk at record cdrop: its
+// fp32 partial sums and count over the DFS prefix before cdrop (walk.cu
+// k_walk_resume continues the same DFS from there with the exact MAC)
+struct __align__(32) ResumeState {
+  float ax, ay, az;
+  uint32_t cnt;
+  uint32_t cdrop;
+  uint32_t pad[3];
+};
+
 struct Workspace {
   float4 *pos4;
   float4 *vel4;
@@ -98,6 +113,8 @@ struct Workspace {
   uint32_t *sort_tilectr; // 8
   float *bbox_part;       // partial min/max per block (8 floats)
   Rec *rec;
+  ResumeState *resume;  // cap_resume entries (queue slots beyond it re-walk from the root)
+  int64_t cap_resume;
   uint32_t *rec_first;
   double4 *rec_mom;
   uint32_t *lvl_list;
@@ -105,7 +122,7 @@ struct Workspace {
 };
 
 struct Layout {
-  int64_t n, cap_rec, cap_int, n_own_max, sort_tiles, scan_tiles;
+  int64_t n, cap_rec, cap_int, n_own_max, sort_tiles, scan_tiles, cap_resume;
   size_t total;
   size_t off[32];
 };

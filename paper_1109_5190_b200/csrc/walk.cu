@@ -20,8 +20,9 @@
 // MAC decisions are exact.  The fast kernel decides with the fp32 thresholds
 // T_acc / T_rej of com.cu (d2_32 > T_acc: accept for sure; d2_32 < T_rej: open
 // for sure).  A lane whose d2_32 falls between them (~1e-6 of the tests) drops
-// out of the fast walk and is queued; k_walk_exact then re-walks those targets
-// alone with the oracle's fp64 test on the ambiguous nodes.  The fast loop thus
+// out of the fast walk at that record and is queued with its partial sums;
+// k_walk_resume then continues each such target's DFS from that record alone,
+// with the oracle's fp64 test on the ambiguous nodes.  The fast loop thus
 // carries no fp64 code and no divergent branch.
 //
 // Interaction (fp32): r2 = d2 + eps^2, f = M rsqrt(r2)^3, a += f (dx, dy, dz):
@@ -50,6 +51,9 @@ struct WalkParams {
   DevStatus *st;
   uint32_t *icount;
   uint32_t *redo;
+  ResumeState *resume;
+  int64_t cap_resume;
+  int need_cont;
   float4 *pos4;
   float4 *vel4;
   float *acc_out;  // mode 0: acc_out[3 uid[s]] (user_order) or acc_out[3 (s - own_lo)]
@@ -122,6 +126,28 @@ __device__ __forceinline__ void finish(const WalkParams &P, const Target &T, dou
   }
 }
 
+// A target whose fp32 MAC test was inconclusive at record cdrop (its resume
+// word is BH_DROP | cdrop) is queued with its fp32 partial sums and count over
+// the DFS prefix before cdrop; k_walk_resume continues the same DFS from
+// cdrop with the oracle's exact test.  `own` = 1 if the count includes the
+// target's own record (the CONT = false kernels accept it with a zero
+// contribution; the resume kernel opens it, as the oracle does).
+__device__ __forceinline__ void push_resume(const WalkParams &P, int64_t t, uint32_t res, float ax, float ay, float az,
+                                            uint32_t cnt, uint32_t own) {
+  const unsigned long long k = atomicAdd(&P.st->n_redo, 1ull);
+  P.redo[k] = (uint32_t)t;
+  if ((int64_t)k < P.cap_resume) {
+    ResumeState r;
+    r.ax = ax;
+    r.ay = ay;
+    r.az = az;
+    r.cnt = cnt - own;
+    r.cdrop = res & ~BH_DROP;
+    r.pad[0] = r.pad[1] = r.pad[2] = 0u;
+    P.resume[k] = r;
+  }
+}
+
 template <int G, bool STATS>
 __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   const uint32_t full = 0xffffffffu;
@@ -188,7 +214,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
       ay = fmaf(f, dy, ay);
       az = fmaf(f, dz, az);
       asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cnt) : "r"((uint32_t)acc));
-      resume = acc ? skip : (amb ? 0xffffffffu : resume);
+      resume = acc ? skip : (amb ? (BH_DROP | cc) : resume);
       uint32_t nxt;
       if (G == 32) {
         nxt = __any_sync(full, opn) ? cc + 1u : skip;
@@ -213,8 +239,8 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
   }
   dax += ax; day += ay; daz += az;
   // warp reductions of the counters
-  // a lane that met an inconclusive MAC test dropped out with resume = ~0u
-  const bool redo = tvalid && resume == 0xffffffffu;
+  // a lane that met an inconclusive MAC test dropped out with resume = BH_DROP | c
+  const bool redo = tvalid && resume >= BH_DROP;
   unsigned long long wc = redo ? 0u : cnt, wo = nop, wi = nit;
   for (int o = 16; o; o >>= 1) {
     wc += __shfl_xor_sync(full, wc, o);
@@ -236,9 +262,8 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
     if (STATS && wi) atomicAdd(&P.st->iters, wi);
   }
   if (!tvalid) return;
-  if (redo) {  // re-walked by k_walk_exact
-    unsigned long long k = atomicAdd(&P.st->n_redo, 1ull);
-    P.redo[k] = (uint32_t)t;
+  if (redo) {  // continued by k_walk_resume
+    push_resume(P, t, resume, (float)dax, (float)day, (float)daz, cnt, 0u);
     return;
   }
   finish(P, T, dax, day, daz, cnt);
@@ -297,12 +322,14 @@ __device__ __forceinline__ void ld_rec(const Rec *p, float4 &cm, uint4 &au) {
 // One target's MAC decision at record cc, as bit masks (few live predicates):
 //   act = cc >= res (and, with CONT, the record does not contain the target)
 //   acc = act & d2 > T_acc      -> interact (f kept), cnt += 1, res = skip
-//   amb = act & !acc & d2 >= T_rej -> inconclusive: res = ~0 (re-walked exactly)
+//   amb = act & !acc & d2 >= T_rej -> inconclusive: res = BH_DROP | cc (the
+//                                   target drops out; k_walk_resume continues it)
 //   opn |= act & d2 < T_rej     -> the lane descends
 // Identical decisions to k_walk / k_walk2.
 __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, float tacc, float trej, uint32_t skip,
                                          uint32_t &resA, uint32_t &resB, uint32_t &cntA, uint32_t &cntB,
                                          uint32_t &opn, float &fA, float &fB) {
+  const uint32_t drop = BH_DROP | cc;
   asm("{\n\t.reg .pred pa, pc, pq, pb, pd, pr, po;\n\t"
       "setp.ge.u32 pa, %9, %0;\n\t"                 // act A
       "setp.gt.and.f32 pc, %10, %12, pa;\n\t"       // acc A
@@ -312,8 +339,8 @@ __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, floa
       "setp.ge.and.f32 pr, %11, %13, pb;\n\t"       // acc-or-amb B
       "@pc add.u32 %2, %2, 1;\n\t"
       "@pd add.u32 %3, %3, 1;\n\t"
-      "@pq selp.b32 %0, %14, 0xffffffff, pc;\n\t"   // acc: skip; amb: ~0 (re-walk)
-      "@pr selp.b32 %1, %14, 0xffffffff, pd;\n\t"
+      "@pq selp.b32 %0, %14, %15, pc;\n\t"   // acc: skip; amb: BH_DROP | cc (dropped out)
+      "@pr selp.b32 %1, %14, %15, pd;\n\t"
       "@!pc mov.b32 %5, 0f00000000;\n\t"
       "@!pd mov.b32 %6, 0f00000000;\n\t"
       "not.pred pq, pq;\n\t"
@@ -323,7 +350,7 @@ __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, floa
       "or.pred po, pa, pb;\n\t"
       "@po mov.b32 %4, 1;\n\t}"
       : "+r"(resA), "+r"(resB), "+r"(cntA), "+r"(cntB), "+r"(opn), "+f"(fA), "+f"(fB)
-      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip));
+      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip), "r"(drop));
 }
 
 #ifndef BH_WALK2_MINB
@@ -427,7 +454,7 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
       float fA, fB;
       up2(mul2(mul2(pk2(cm.w, cm.w), mul2(INV, INV)), INV), fA, fB);
       // per-target MAC (identical decisions to k_walk); an inconclusive fp32
-      // test drops the target out (resume = ~0): k_walk_exact re-walks it
+      // test drops the target out (resume = BH_DROP | c): k_walk_resume continues it
       if (CONT) {
         // a record containing the target is opened, never accepted (NaN
         // distance: every comparison is false)
@@ -459,8 +486,8 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
   bool redo[TPL];
 #pragma unroll
   for (int k = 0; k < TPL; k++) {
-    redo[k] = v[k] && res[k] == 0xffffffffu;
-    if (!CONT) cnt[k] -= v[k] ? 1u : 0u;  // own record: "accepted", zero contribution
+    redo[k] = v[k] && res[k] >= BH_DROP;
+    if (!CONT && !redo[k]) cnt[k] -= v[k] ? 1u : 0u;  // own record: "accepted", zero contribution
     wc += redo[k] ? 0u : cnt[k];
   }
   for (int o = 16; o; o >>= 1) wc += __shfl_xor_sync(full, wc, o);
@@ -471,7 +498,9 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
 #pragma unroll
   for (int k = 0; k < TPL; k++) {
     if (!v[k]) continue;
-    if (redo[k]) P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)(tbase + (int64_t)k * GL);
+    if (redo[k])
+      push_resume(P, tbase + (int64_t)k * GL, res[k], ax[k], ay[k], az[k], cnt[k],
+                  (!CONT && Li[k] < (res[k] & ~BH_DROP)) ? 1u : 0u);
     else finish(P, T[k], (double)ax[k], (double)ay[k], (double)az[k], cnt[k]);
   }
 }
@@ -541,10 +570,10 @@ __global__ void __launch_bounds__(256, (NP == 1 || !PERSIST) ? 4 : 3) k_walk_lan
         for (int k = 0; k < TPL; k++) {
           const int64_t t = g * GT + gl * TPL + k;
           if (t >= P.n_targets) continue;
-          if (!CONT) cnt[k] -= 1u;  // own record: "accepted", zero contribution
-          if (res[k] == 0xffffffffu) {
-            P.redo[atomicAdd(&P.st->n_redo, 1ull)] = (uint32_t)t;
+          if (res[k] >= BH_DROP) {
+            push_resume(P, t, res[k], ax[k], ay[k], az[k], cnt[k], (!CONT && Li[k] < (res[k] & ~BH_DROP)) ? 1u : 0u);
           } else {
+            if (!CONT) cnt[k] -= 1u;  // own record: "accepted", zero contribution
             wc += cnt[k];
             finish(P, load_target(P, t), (double)ax[k], (double)ay[k], (double)az[k], cnt[k]);
           }
@@ -672,136 +701,144 @@ __global__ void __launch_bounds__(256, (NP == 1 || !PERSIST) ? 4 : 3) k_walk_lan
   }
 }
 
-// Exact walk of the queued targets.  One WARP per target: the node set a target
-// interacts with does not depend on the visiting order, so the warp expands the
-// target's frontier 32 nodes at a time from a LIFO stack in shared memory
-// (opened nodes push their children in a fixed, ballot-ranked order) and tests
-// each node with the fp32 filter, falling back to the oracle's fp64 formula on
-// the ambiguous ones.  Partial sums: fp64 per lane, reduced in lane order.  A
-// stack overflow (never seen; bounded by ~8 x depth x 32) falls back to the
-// one-lane DFS below.
-constexpr int EXACT_WARPS = 4;
-constexpr int EXACT_STACK = 2048;
+// Continuation of the targets that dropped out of the fast walk (k_walk_resume).
+// One WARP per queued target.  A DFS segment (x, b) -- "visit x, then go on at
+// skip(x) while below b" -- splits into x itself, the segment (x+1, skip(x)) of
+// its subtree if x is opened, and the segment (skip(x), b) of what follows; the
+// target's remaining walk is the segment (cdrop, Wn).  The warp pops up to 32
+// segments from a LIFO in shared memory, each lane tests its node with the fp32
+// filter (the oracle's fp64 formula, exact_accept, on inconclusive tests;
+// records containing the target are opened, reading L5), interacts or pushes
+// the subtree segment, and pushes the follow-on segment (ballot-ranked, so the
+// order is deterministic).  Lane partials are fp64, reduced in lane order and
+// added to the fast walk's fp32 prefix.  Queue slots beyond the resume-state
+// capacity restart at (0, Wn) with zero partials.  A full stack (never seen;
+// bounded by ~2 x 32 x depth) hands the remaining segments to lane 0, which
+// walks each one stacklessly.
+constexpr int RESUME_WARPS = 4;
+constexpr int RESUME_STACK = 1024;
 
-__device__ void exact_dfs_one_lane(const WalkParams &P, const Target &T, uint32_t Wn, double Ld, double &dax,
-                                   double &day, double &daz, uint32_t &cnt, uint32_t &fb, uint32_t &nop) {
-  uint32_t c = 0;
-  while (c < Wn) {
-    const float4 cm = P.rec[c].cm;
-    const uint4 au = P.rec[c].aux;
-    const float dx = cm.x - T.me.x, dy = cm.y - T.me.y, dz = cm.z - T.me.z;
-    const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    const bool cont = (c <= T.Li) & (au.z > T.Li);
-    bool acc = !cont & (d2 > __uint_as_float(au.x));
-    if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
-      acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
-      fb++;
-    }
-    if (acc) {
-      const float inv = rsqrt_fast(d2 + P.eps2);
-      const float f = cm.w * (inv * inv) * inv;
-      dax += (double)(f * dx);
-      day += (double)(f * dy);
-      daz += (double)(f * dz);
-      cnt++;
-      c = au.z;
-    } else {
-      nop++;
-      c = c + 1u;
-    }
+struct ResumeAcc {
+  double ax, ay, az;
+  uint32_t cnt, fb, nop;
+};
+
+// test node c for target T; returns true if accepted (and accumulates)
+__device__ __forceinline__ bool resume_visit(const WalkParams &P, const Target &T, double Ld, uint32_t c,
+                                             uint32_t &skip, ResumeAcc &A) {
+  const float4 cm = P.rec[c].cm;
+  const uint4 au = P.rec[c].aux;
+  skip = au.z;
+  const float dx = __fsub_rn(cm.x, T.me.x), dy = __fsub_rn(cm.y, T.me.y), dz = __fsub_rn(cm.z, T.me.z);
+  const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+  const bool cont = (c <= T.Li) & (au.z > T.Li);
+  bool acc = !cont & (d2 > __uint_as_float(au.x));
+  if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
+    acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
+    A.fb++;
   }
+  if (acc) {
+    const float inv = rsqrt_fast(__fadd_rn(d2, P.eps2));
+    const float f = __fmul_rn(__fmul_rn(cm.w, __fmul_rn(inv, inv)), inv);
+    A.ax += (double)__fmul_rn(f, dx);
+    A.ay += (double)__fmul_rn(f, dy);
+    A.az += (double)__fmul_rn(f, dz);
+    A.cnt++;
+  } else {
+    A.nop++;
+  }
+  return acc;
 }
 
-__global__ void __launch_bounds__(32 * EXACT_WARPS) k_walk_exact(const WalkParams P) {
-  __shared__ uint32_t stack[EXACT_WARPS][EXACT_STACK];
+__global__ void __launch_bounds__(32 * RESUME_WARPS) k_walk_resume(const WalkParams P) {
+  __shared__ uint2 stack[RESUME_WARPS][RESUME_STACK];
   if (P.st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t full = 0xffffffffu;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t *stk = stack[w];
+  uint2 *stk = stack[w];
   const uint32_t Wn = P.st->n_records;
   const unsigned long long nredo = P.st->n_redo;
   const double Ld = (double)P.st->L;
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-  for (unsigned long long k = blockIdx.x * (unsigned long long)EXACT_WARPS + w; k < nredo;
-       k += (unsigned long long)gridDim.x * EXACT_WARPS) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)RESUME_WARPS + w; k < nredo;
+       k += (unsigned long long)gridDim.x * RESUME_WARPS) {
     const Target T = load_target(P, P.redo[k]);
-    double dax = 0.0, day = 0.0, daz = 0.0;
-    uint32_t cnt = 0, fb = 0, nop = 0;
-    uint32_t sp = 1;
-    if (lane == 0) stk[0] = 0u;  // the root
+    float pax = 0.f, pay = 0.f, paz = 0.f;
+    uint32_t pcnt = 0, c0 = 0;
+    if ((int64_t)k < P.cap_resume) {
+      const ResumeState r = P.resume[k];
+      pax = r.ax;
+      pay = r.ay;
+      paz = r.az;
+      pcnt = r.cnt;
+      c0 = r.cdrop;
+    }
+    ResumeAcc A = {0.0, 0.0, 0.0, 0u, 0u, 0u};
+    uint32_t sp = 0;
+    if (c0 < Wn) {
+      if (lane == 0) stk[0] = make_uint2(c0, Wn);
+      sp = 1;
+    }
     bool overflow = false;
     __syncwarp();
     while (sp > 0 && !overflow) {
       const uint32_t nt = sp < 32u ? sp : 32u;
       const uint32_t base = sp - nt;
       const bool have = (uint32_t)lane < nt;
-      const uint32_t c = have ? stk[base + lane] : 0u;
+      const uint2 seg = have ? stk[base + lane] : make_uint2(0u, 0u);
       __syncwarp();
       sp = base;
-      bool opn = false;
-      uint32_t skip = 0;
+      uint2 p1 = make_uint2(0u, 0u), p2 = make_uint2(0u, 0u);
+      bool push1 = false, push2 = false;
       if (have) {
-        const float4 cm = P.rec[c].cm;
-        const uint4 au = P.rec[c].aux;
-        skip = au.z;
-        const float dx = cm.x - T.me.x, dy = cm.y - T.me.y, dz = cm.z - T.me.z;
-        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        const bool cont = (c <= T.Li) & (au.z > T.Li);
-        bool acc = !cont & (d2 > __uint_as_float(au.x));
-        if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
-          acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
-          fb++;
-        }
-        if (acc) {
-          const float inv = rsqrt_fast(d2 + P.eps2);
-          const float f = cm.w * (inv * inv) * inv;
-          dax += (double)(f * dx);
-          day += (double)(f * dy);
-          daz += (double)(f * dz);
-          cnt++;
-        } else {
-          nop++;
-          opn = skip > c + 1u;  // has children
-        }
+        uint32_t skip;
+        const bool acc = resume_visit(P, T, Ld, seg.x, skip, A);
+        push1 = skip < seg.y;                          // the follow-on segment
+        p1 = make_uint2(skip, seg.y);
+        push2 = !acc && seg.x + 1u < skip;             // the opened node's subtree
+        p2 = make_uint2(seg.x + 1u, skip);
       }
-      // push the children of every opened node, one child per lane per round,
-      // at ballot-ranked positions (deterministic order)
-      uint32_t ch = c + 1u;
-      for (;;) {
-        const bool push = opn && ch < skip;
-        const uint32_t b = __ballot_sync(full, push);
-        if (!b) break;
-        if (sp + __popc(b) > EXACT_STACK) { overflow = true; break; }
-        if (push) {
-          stk[sp + __popc(b & lt)] = ch;
-          ch = P.rec[ch].aux.z;
-        }
-        sp += __popc(b);
+      const uint32_t b1 = __ballot_sync(full, push1), b2 = __ballot_sync(full, push2);
+      const uint32_t tot = __popc(b1) + __popc(b2);
+      if (sp + tot > RESUME_STACK) {  // warp-uniform; lane 0 redoes the target below
+        overflow = true;
+        break;
       }
+      // follow-on segments first (popped last), subtree segments on top: the
+      // LIFO then goes depth-first
+      if (push1) stk[sp + __popc(b1 & lt)] = p1;
+      if (push2) stk[sp + __popc(b1) + __popc(b2 & lt)] = p2;
+      sp += tot;
       __syncwarp();
     }
     // reduce the lane partials in lane order
     for (int o = 16; o; o >>= 1) {
-      dax += __shfl_xor_sync(full, dax, o);
-      day += __shfl_xor_sync(full, day, o);
-      daz += __shfl_xor_sync(full, daz, o);
-      cnt += __shfl_xor_sync(full, cnt, o);
-      fb += __shfl_xor_sync(full, fb, o);
-      nop += __shfl_xor_sync(full, nop, o);
+      A.ax += __shfl_xor_sync(full, A.ax, o);
+      A.ay += __shfl_xor_sync(full, A.ay, o);
+      A.az += __shfl_xor_sync(full, A.az, o);
+      A.cnt += __shfl_xor_sync(full, A.cnt, o);
+      A.fb += __shfl_xor_sync(full, A.fb, o);
+      A.nop += __shfl_xor_sync(full, A.nop, o);
     }
-    if (overflow) {  // lane 0 redoes the target depth-first
-      dax = day = daz = 0.0;
-      cnt = fb = nop = 0;
-      if (lane == 0) exact_dfs_one_lane(P, T, Wn, Ld, dax, day, daz, cnt, fb, nop);
+    if (overflow) {  // lane 0 walks the whole remaining segment stacklessly
+      A = ResumeAcc{0.0, 0.0, 0.0, 0u, 0u, 0u};
+      if (lane == 0) {
+        uint32_t c = c0;
+        while (c < Wn) {
+          uint32_t skip;
+          c = resume_visit(P, T, Ld, c, skip, A) ? skip : c + 1u;
+        }
+      }
     }
     if (lane == 0) {
+      const uint32_t cnt = pcnt + A.cnt;
       atomicAdd(&P.st->interactions, (unsigned long long)cnt);
       atomicAdd(&P.st->interactions_cum, (unsigned long long)cnt);
-      atomicAdd(&P.st->fallbacks, (unsigned long long)fb);
-      atomicAdd(&P.st->opens, (unsigned long long)nop);
-      atomicAdd(&P.st->opens_cum, (unsigned long long)nop);
-      finish(P, T, dax, day, daz, cnt);
+      atomicAdd(&P.st->fallbacks, (unsigned long long)A.fb);
+      atomicAdd(&P.st->opens, (unsigned long long)A.nop);
+      atomicAdd(&P.st->opens_cum, (unsigned long long)A.nop);
+      finish(P, T, (double)pax + A.ax, (double)pay + A.ay, (double)paz + A.az, cnt);
     }
     __syncwarp();
   }
@@ -819,6 +856,9 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.st = W.status;
   P.icount = W.icount;
   P.redo = W.redo;
+  P.resume = W.resume;
+  P.cap_resume = W.cap_resume;
+  P.need_cont = a.need_cont;
   P.pos4 = W.pos4;
   P.vel4 = W.vel4;
   P.acc_out = a.acc_out;
@@ -951,10 +991,11 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   }
 #undef BH_WALK_CASE
   }
-  // the exact re-walk: a fixed grid of warps, grid-stride over the device-side queue
-  int64_t eg = (a.n_targets + EXACT_WARPS - 1) / EXACT_WARPS;
+  // the continuation of dropped-out targets: a fixed grid, grid-stride over the
+  // device-side queue (lanes dense in queue order)
+  int64_t eg = (a.n_targets + RESUME_WARPS - 1) / RESUME_WARPS;
   if (eg > 148 * 8) eg = 148 * 8;
-  k_walk_exact<<<(unsigned)eg, 32 * EXACT_WARPS, 0, s>>>(P);
+  k_walk_resume<<<(unsigned)eg, 32 * RESUME_WARPS, 0, s>>>(P);
   return cudaGetLastError();
 }
 
