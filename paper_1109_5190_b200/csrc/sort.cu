@@ -26,6 +26,7 @@ constexpr int SORT_WARPS = SORT_BLOCK / 32;
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_PRE = 2u << 30;
 constexpr uint32_t VAL_MASK = (1u << 30) - 1;
+constexpr int LOOKBACK = 16;  // status words per look-back round trip
 
 struct SortSmem {
   unsigned long long keys[SORT_TILE];
@@ -147,14 +148,28 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_onesweep(const unsigned long lon
     st_relaxed(my, FLAG_PRE | tot);
   } else {
     st_relaxed(my, FLAG_AGG | tot);
+    // look back LB tiles per round trip: the nearest inclusive prefix is
+    // usually a whole wave of resident tiles back, so one status word per
+    // round trip would serialise the pass on load latency
     int64_t t = (int64_t)tile - 1;
     for (;;) {
-      uint32_t s = ld_relaxed(status + (size_t)t * SORT_RADIX + dd);
-      uint32_t f = s & ~VAL_MASK;
-      if (f == 0) continue;
-      excl += s & VAL_MASK;
-      if (f == FLAG_PRE) break;
-      --t;
+      uint32_t sv[LOOKBACK];
+#pragma unroll
+      for (int i = 0; i < LOOKBACK; i++)
+        sv[i] = t - i >= 0 ? ld_relaxed(status + (size_t)(t - i) * SORT_RADIX + dd) : FLAG_PRE;
+      int used = 0;
+      bool done = false;
+#pragma unroll
+      for (int i = 0; i < LOOKBACK; i++) {
+        if (done || used < i) continue;  // stopped at an unpublished word
+        const uint32_t f = sv[i] & ~VAL_MASK;
+        if (f == 0) continue;
+        excl += sv[i] & VAL_MASK;
+        used = i + 1;
+        done = f == FLAG_PRE;
+      }
+      if (done) break;
+      t -= used;
     }
     st_relaxed(my, FLAG_PRE | (excl + tot));
   }
