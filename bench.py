@@ -327,19 +327,21 @@ def ours_arm(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(workload_config(cfg, m, p, v), parallelism=f"morton-range x{world}",
-                           walk_group=args.walk_group or 32),
+                           walk_group=args.walk_group,
+                           walk_kernel=("k_walk2<4,1>: 8-target groups, 4 lanes x 2 targets" if args.walk_group == 0
+                                        else f"walk_group {args.walk_group} (include/bh.h)")),
             "particles_per_s": particles_per_s,
             "interactions_per_step": inter / args.steps,
             "fp32_peak_frac": achieved_tf / peak,
-            "roofline": {"bound": "alu", "kernel": "k_walk (K6+K7)", "achieved": achieved_tf, "peak": peak,
+            "roofline": {"bound": "alu", "kernel": "K6+K7 walk phase: k_walk2 + k_walk_resume", "achieved": achieved_tf,
+                         "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
                          "peak_source": f"derived: 2 flop x 128 FP32 lanes x {sms} SMs x {sm_max:.0f} MHz "
                                         "(sm_max_mhz of MEASURED_PEAKS.json; B200_PROFILING.md)",
                          "flops_per_launch": flops_walk_launch, "launch_ms": walk_ms,
                          "flop_model": "18 per interaction + 8 per opened node (opens/interaction ratio from an "
-                                       "untimed stats walk on the final state)",
-                         "simd_efficiency": (sts["interactions"] + sts["opens"]) / max(1, sts["lane_iters"])},
+                                       "untimed stats walk on the final state)"},
             "hbm_stages": {"sort_GBps": sort_gbs, "sort_bytes_model": "8 passes x 24 B/particle",
                            "hbm_peak_GBps": peaks.get("hbm_gbs")},
             "phase_ms_per_step": phase_ms,

@@ -42,7 +42,7 @@ def launches(path):
         d = dict(zip(hdr, r))
         if d["Metric Name"] != "gpu__time_duration.sum":
             continue
-        name = d["Kernel Name"].split("(")[0].replace("void ", "")
+        name = d["Kernel Name"].split("(")[0].replace("void ", "").strip()
         tot[name] += float(d["Metric Value"].replace(",", "")) * UNIT_NS.get(d["Metric Unit"], 1e-6)
         cnt[name] += 1
     return tot, cnt
@@ -95,6 +95,8 @@ def main():
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--command", default="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline")
+    ap.add_argument("--exclude", default="k_walk<32, 1>",
+                    help="semicolon-separated kernels launched outside the timed steps (shares also shown without them)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     md = [f"# ncu summary, round {a.round}", "", f"Workload: BASELINE {a.workload}; command `{a.command}` on one B200 "
@@ -106,10 +108,19 @@ def main():
         T = sum(tot.values())
         md += ["## Launch list (`--metrics gpu__time_duration.sum`, cold-cache and serialised: compare shares)", "",
                "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+        excl = [x.strip() for x in a.exclude.split(";") if x.strip()]
+        Ts = sum(v for k, v in tot.items() if k not in excl)
+        md[-2] = md[-2].replace("| share |", "| share | share of the step kernels |")
+        md[-1] = "|---|---|---|---|---|"
         for k, v in sorted(tot.items(), key=lambda t: -t[1]):
-            md.append(f"| `{k}` | {cnt[k]} | {v:.3f} | {100 * v / T:.2f}% |")
+            step = "untimed helper" if k in excl else f"{100 * v / Ts:.2f}%"
+            md.append(f"| `{k}` | {cnt[k]} | {v:.3f} | {100 * v / T:.2f}% | {step} |")
+        md.append("")
+        md.append(f"Excluded from the step shares: {', '.join(excl) or 'nothing'} (launched outside bh_step, e.g. "
+                  "the untimed stats walk bench.py runs once for the flop model).")
         md.append("")
         js["launch_share"] = {k: v / T for k, v in tot.items()}
+        js["launch_share_step"] = {k: v / Ts for k, v in tot.items() if k not in excl}
     for spec in a.rep:
         key, rep = spec.split("=", 1)
         d = details(rep)
