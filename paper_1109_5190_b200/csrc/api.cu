@@ -497,6 +497,13 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   memset(ctx->prof_ms, 0, sizeof ctx->prof_ms);
   memset(ctx->prof_launches, 0, sizeof ctx->prof_launches);
   bind_workspace(lay, p->workspace, ctx->W);
+  // test hooks: a smaller resume-state capacity / resume stack exercises the
+  // walk's rare paths (queue slots restarting from the root, stack overflow)
+  if (getenv("BH_RESUME_CAP")) {
+    const long long c = atoll(getenv("BH_RESUME_CAP"));
+    if (c >= 0 && c < ctx->W.cap_resume) ctx->W.cap_resume = c;
+  }
+  ctx->W.resume_stack = getenv("BH_RESUME_STACK") ? atoi(getenv("BH_RESUME_STACK")) : 0;
   const int64_t n = p->n;
   ctx->own_lo = n * p->rank / p->world;
   ctx->own_hi = n * (p->rank + 1) / p->world;

@@ -115,6 +115,7 @@ struct Workspace {
   Rec *rec;
   ResumeState *resume;  // cap_resume entries (queue slots beyond it re-walk from the root)
   int64_t cap_resume;
+  int resume_stack;     // 0: the full resume LIFO; > 0: a smaller one (test hook)
   uint32_t *rec_first;
   double4 *rec_mom;
   uint32_t *lvl_list;

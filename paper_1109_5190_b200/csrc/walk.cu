@@ -53,6 +53,7 @@ struct WalkParams {
   uint32_t *redo;
   ResumeState *resume;
   int64_t cap_resume;
+  int resume_stack;
   int need_cont;
   float4 *pos4;
   float4 *vel4;
@@ -801,7 +802,7 @@ __global__ void __launch_bounds__(32 * RESUME_WARPS) k_walk_resume(const WalkPar
       }
       const uint32_t b1 = __ballot_sync(full, push1), b2 = __ballot_sync(full, push2);
       const uint32_t tot = __popc(b1) + __popc(b2);
-      if (sp + tot > RESUME_STACK) {  // warp-uniform; lane 0 redoes the target below
+      if (sp + tot > (uint32_t)P.resume_stack) {  // warp-uniform; lane 0 redoes the target below
         overflow = true;
         break;
       }
@@ -858,6 +859,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.redo = W.redo;
   P.resume = W.resume;
   P.cap_resume = W.cap_resume;
+  P.resume_stack = W.resume_stack > 0 && W.resume_stack < RESUME_STACK ? W.resume_stack : RESUME_STACK;
   P.need_cont = a.need_cont;
   P.pos4 = W.pos4;
   P.vel4 = W.vel4;

@@ -328,3 +328,22 @@ def test_step_graph_matches_direct_launches(BH, monkeypatch):
     g.step(2)
     d.step(2)
     assert np.array_equal(g.get_state()[0], d.get_state()[0])
+
+
+@pytest.mark.parametrize("hook", [{"BH_RESUME_CAP": "4"}, {"BH_RESUME_STACK": "40"}])
+def test_resume_rare_paths(BH, monkeypatch, hook):
+    """Targets whose fp32 MAC test was inconclusive continue in k_walk_resume.
+    Its rare paths, forced by test hooks: queue slots beyond the resume-state
+    capacity restart from the root; a full segment stack hands the target to
+    one lane's stackless walk.  Both must still give the oracle's counts and
+    forces."""
+    for k, v in hook.items():
+        monkeypatch.setenv(k, v)
+    m, p, v = bhgen.generate("cfg3", n=300000)
+    prm = bhgen.params("cfg3")
+    bh = BH(m, p, v, **prm)
+    bh.build_tree()
+    o = _oracle(m, p, v, prm)
+    check_step0(bh, o, m.shape[0])
+    st = bh.get_stats()
+    assert st["redo_targets"] > 4, "the input must exercise the resume path"
