@@ -94,7 +94,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
   L.n_own_max = (n + world - 1) / world + 1;
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-  size_t sz[22] = {
+  size_t sz[23] = {
       sizeof(DevStatus),                       // 0 status
       (size_t)n * 16,                          // 1 pos4
       (size_t)L.n_own_max * 16,                // 2 vel4
@@ -117,9 +117,10 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
       (size_t)L.cap_rec * 32,                  // 19 rec_mom
       (size_t)L.cap_int * 4,                   // 20 lvl_list
       (size_t)n * 4,                           // 21 redo list
+      ((size_t)n / 8 + 64) * 4,                // 22 walk group costs (8-target groups)
   };
   size_t off = 0;
-  for (int i = 0; i < 22; i++) {
+  for (int i = 0; i < 23; i++) {
     L.off[i] = off;
     off += align_up(sz[i]);
   }
@@ -154,6 +155,7 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.rec_mom = (double4 *)(b + L.off[19]);
   W.lvl_list = (uint32_t *)(b + L.off[20]);
   W.redo = (uint32_t *)(b + L.off[21]);
+  W.gcost = (uint32_t *)(b + L.off[22]);
 }
 
 // ---------------------------------------------------------------- small kernels
@@ -561,6 +563,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
       if (cudaMemsetAsync(ctx->W.vel4, 0, (size_t)own_n * 16, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
     }
     if (cudaMemsetAsync(ctx->W.icount, 0, (size_t)n * 4, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
+    if (cudaMemsetAsync(ctx->W.gcost, 0, ((size_t)n / 8 + 64) * 4, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
     st = do_sync(ctx);
   } while (0);
   if (st != BH_OK) {

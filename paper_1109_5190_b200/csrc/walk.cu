@@ -36,6 +36,7 @@
 // L8), x += v dt, written in place to pos4 / vel4 of the particle's storage slot
 // (the walk reads positions from the records, never from pos4).
 #include <math.h>
+#include <stdlib.h>
 
 #include "bh_internal.cuh"
 
@@ -58,6 +59,7 @@ struct WalkParams {
   float4 *pos4;
   float4 *vel4;
   float *acc_out;  // mode 0: acc_out[3 uid[s]] (user_order) or acc_out[3 (s - own_lo)]
+  uint32_t *gcost;  // k_walk2<4,1>: last-walk iterations per 8-target group (or null)
   int user_order;
   int64_t n_targets;
   int use_targets;
@@ -392,9 +394,34 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
     __syncthreads();
     chunk = s_chunk;
   }
-  const int64_t wbase = (chunk * (int64_t)blockDim.x + (threadIdx.x & ~31)) * TPL;
+  // Group order.  The block's 256 / GL groups are dealt to its warps in
+  // descending order of their last-walk cost (union-walk iterations, gcost):
+  // a warp runs until its slowest group is done, so warps of similar groups
+  // idle less (the groups themselves -- which targets walk together -- do not
+  // change, hence neither do the results).  Without costs: Morton order.
+  constexpr int GPB = 256 / GL;  // groups per block
   const int gi = lane / GL, gl = lane % GL;
-  const int64_t tbase = wbase + (int64_t)gi * TPL * GL + gl;
+  int lg = (threadIdx.x >> 5) * (32 / GL) + gi;  // local group of this lane
+  if (P.gcost) {
+    __shared__ uint32_t s_cost[GPB], s_perm[GPB];
+    const int64_t g0 = (int64_t)chunk * GPB;
+    const int64_t ngroups = (P.n_targets + GL * TPL - 1) / (GL * TPL);
+    if (threadIdx.x < GPB) s_cost[threadIdx.x] = g0 + threadIdx.x < ngroups ? P.gcost[g0 + threadIdx.x] : 0u;
+    __syncthreads();
+    if (threadIdx.x < GPB) {
+      const uint32_t ci = s_cost[threadIdx.x];
+      int r = 0;
+      for (int j = 0; j < GPB; j++) {
+        const uint32_t cj = s_cost[j];
+        r += (cj > ci) | ((cj == ci) & (j < (int)threadIdx.x));
+      }
+      s_perm[r] = threadIdx.x;
+    }
+    __syncthreads();
+    lg = (int)s_perm[lg];
+  }
+  const int64_t gidx = (int64_t)chunk * GPB + lg;  // global group index
+  const int64_t tbase = gidx * (GL * TPL) + gl;
   Target T[TPL];
   bool v[TPL];
   bool anyv = false;
@@ -429,9 +456,14 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
   uint32_t gmask2 = gmask;
   asm volatile("" : "+r"(gmask2));  // a plain register: the group test is one LOP3
   uint32_t c = gvalid ? 0u : Wn;
+  uint32_t git = 0;  // union-walk trips (2 visits) of this lane's group (its cost)
   // a finished group parks on the sentinel record Wn (T_acc = T_rej = +inf,
   // skip = Wn: nothing is accepted or queued there) until the warp is done
+  // two visits per trip: the exit vote and the cost counter run once per trip
+  // (a parked group stays on the sentinel, so the extra visit is harmless)
   if (__any_sync(full, c < Wn)) for (;;) {
+#pragma unroll
+   for (int u = 0; u < 2; u++) {
     const uint32_t cc = c;
     float4 cm;
     uint4 au;
@@ -476,13 +508,17 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
           : "+f"(az[a]), "+f"(az[b]) : "l"(FF.v), "l"(DZ.v));
     }
     if (GL == 32) {
-      c = __any_sync(full, opn != 0u) ? cc + 1u : skip;
+      c = min(__any_sync(full, opn != 0u) ? cc + 1u : skip, Wn);
     } else {
       const uint32_t nxt = (__ballot_sync(full, opn != 0u) & gmask2) ? cc + 1u : skip;
       c = min(nxt, Wn);
     }
-    if (!__any_sync(full, c < Wn)) break;
+   }
+    const bool live = c < Wn;
+    git += live ? 1u : 0u;
+    if (!__any_sync(full, live)) break;
   }
+  if (P.gcost && gl == 0 && anyv) P.gcost[gidx] = git;
   unsigned long long wc = 0;
   bool redo[TPL];
 #pragma unroll
@@ -857,6 +893,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.st = W.status;
   P.icount = W.icount;
   P.redo = W.redo;
+  P.gcost = (!a.stats && a.group == 0 && !getenv("BH_NO_GROUP_ORDER")) ? W.gcost : nullptr;
   P.resume = W.resume;
   P.cap_resume = W.cap_resume;
   P.resume_stack = W.resume_stack > 0 && W.resume_stack < RESUME_STACK ? W.resume_stack : RESUME_STACK;
