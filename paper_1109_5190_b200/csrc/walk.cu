@@ -59,7 +59,7 @@ struct WalkParams {
   float4 *pos4;
   float4 *vel4;
   float *acc_out;  // mode 0: acc_out[3 uid[s]] (user_order) or acc_out[3 (s - own_lo)]
-  uint32_t *gcost;  // k_walk2<4,1>: last-walk iterations per 8-target group (or null)
+  uint32_t *gcost;  // k_walk2: last-walk trips per target group (or null)
   int user_order;
   int64_t n_targets;
   int use_targets;
@@ -356,6 +356,9 @@ __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, floa
       : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip), "r"(drop));
 }
 
+#ifndef BH_WALK2_UNROLL
+#define BH_WALK2_UNROLL 2
+#endif
 #ifndef BH_WALK2_MINB
 #define BH_WALK2_MINB 5
 #endif
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
   // (a parked group stays on the sentinel, so the extra visit is harmless)
   if (__any_sync(full, c < Wn)) for (;;) {
 #pragma unroll
-   for (int u = 0; u < 2; u++) {
+   for (int u = 0; u < BH_WALK2_UNROLL; u++) {
     const uint32_t cc = c;
     float4 cm;
     uint4 au;
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(256, (NP == 1 || !PERSIST) ? 4 : 3) k_walk_lan
       if (__all_sync(full, parked)) break;
     }
 #pragma unroll 2
-    for (int u = 0; u < 2; u++) {
+    for (int u = 0; u < BH_WALK2_UNROLL; u++) {
       const uint32_t cc = c;
       float4 cm;
       uint4 au;
@@ -893,7 +896,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.st = W.status;
   P.icount = W.icount;
   P.redo = W.redo;
-  P.gcost = (!a.stats && a.group == 0 && !getenv("BH_NO_GROUP_ORDER")) ? W.gcost : nullptr;
+  P.gcost = (!a.stats && !getenv("BH_NO_GROUP_ORDER")) ? W.gcost : nullptr;
   P.resume = W.resume;
   P.cap_resume = W.cap_resume;
   P.resume_stack = W.resume_stack > 0 && W.resume_stack < RESUME_STACK ? W.resume_stack : RESUME_STACK;
