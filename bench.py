@@ -282,8 +282,12 @@ def ours_arm(args):
     clocks = clk.summary()
     traffic, traffic_src = load_traffic("walk", f"{cfg.name}")
     phase_ms = {k: vv / args.steps for k, vv in prof["ms"].items()}
-    sort_bytes = 8 * 24 * cfg.n  # 8 passes x (8 B key + 4 B id) read + written
-    sort_gbs = sort_bytes / (phase_ms["sort"] / 1e3) / 1e9 if phase_ms["sort"] > 0 else None
+    # keys + sort phase: the near-sorted path (previous order) moves 88 B per key
+    # (K1' 32, mark 8, split 24, merge 24) + the out-of-order keys' radix passes;
+    # the full path 32 B (K1) + 8 passes x (8 B key + 4 B id) read + written
+    near = st1.get("near_sorted", True)
+    sort_bytes = (88 if near else 32 + 8 * 24) * cfg.n
+    sort_gbs = sort_bytes / (phase_ms["keys_sort"] / 1e3) / 1e9 if phase_ms["keys_sort"] > 0 else None
     launches = sum(prof["launches"].values())
 
     # e2e: through the public API with host buffers, copies inside the timed region
@@ -342,7 +346,9 @@ def ours_arm(args):
                          "flops_per_launch": flops_walk_launch, "launch_ms": walk_ms,
                          "flop_model": "18 per interaction + 8 per opened node (opens/interaction ratio from an "
                                        "untimed stats walk on the final state)"},
-            "hbm_stages": {"sort_GBps": sort_gbs, "sort_bytes_model": "8 passes x 24 B/particle",
+            "hbm_stages": {"keys_sort_GBps": sort_gbs,
+                           "keys_sort_bytes_model": ("near-sorted path: 88 B/particle + the out-of-order keys' passes"
+                                                     if near else "K1 32 B + 8 passes x 24 B per particle"),
                            "hbm_peak_GBps": peaks.get("hbm_gbs")},
             "phase_ms_per_step": phase_ms,
             "mac_fallbacks_last_step": st1["mac_fallbacks"],

@@ -171,13 +171,18 @@ typedef struct {
     int64_t interactions_cum; /* all walks since bh_create                        */
     int64_t opens_cum;
     int64_t lane_iters;     /* last walk: traversal-loop iterations x lanes (SIMD slots) */
-    int64_t redo_targets;   /* last walk: targets re-walked with the exact fp64 MAC        */
+    int64_t redo_targets;   /* last walk: targets whose fp32 MAC test was inconclusive,
+                               continued with the exact fp64 test (k_walk_resume)        */
+    int64_t near_sorted;    /* last build: 1 if the sort took the near-sorted path (keys
+                               in the previous build's order, out-of-order keys sorted
+                               apart and merged), 0 if the full radix sort ran           */
+    int64_t sort_bad_keys;  /* last build, near-sorted path: keys out of local order     */
 } bh_stats;
 bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);
 
 /* Per-phase device time (CUDA events on the ctx stream), accumulated over the
- * calls made while profiling is on.  Phases: 0 bbox+keys, 1 sort, 2 tree,
- * 3 moments, 4 walk(+integrate), 5 exchange.  ms[6], launches[6]. */
+ * calls made while profiling is on.  Phases: 0 bbox (root cube), 1 keys + sort,
+ * 2 tree, 3 moments, 4 walk(+integrate), 5 exchange.  ms[6], launches[6]. */
 bh_status bh_set_profiling(bh_ctx *ctx, int enable);
 bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *calls);
 

@@ -22,7 +22,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bh.h")
 
 BH_OK, BH_ERR_ARG, BH_ERR_CUDA, BH_ERR_OOM, BH_ERR_STATE, BH_ERR_NONFINITE, BH_ERR_NCCL = 0, -1, -2, -3, -4, -5, -6
 BH_HOST, BH_DEVICE = 0, 1
-PHASES = ("bbox_keys", "sort", "tree", "moments", "walk", "exchange")
+PHASES = ("bbox", "keys_sort", "tree", "moments", "walk", "exchange")
 
 
 class BhParams(C.Structure):
@@ -59,6 +59,8 @@ class BhStats(C.Structure):
         ("opens_cum", C.c_int64),
         ("lane_iters", C.c_int64),
         ("redo_targets", C.c_int64),
+        ("near_sorted", C.c_int64),
+        ("sort_bad_keys", C.c_int64),
     ]
 
 

@@ -42,6 +42,7 @@ struct bh_ctx {
   cudaGraphExec_t step_graph[2];  // [0]: half kick (first step), [1]: full kick
   int num_sms;
   int sort_buf;
+  int near_sort;        // 1: try the near-sorted path each build (nearsort.cu)
   DevStatus *hstatus;  // pinned
   cudaEvent_t status_ev;
   bool status_pending;
@@ -346,13 +347,16 @@ static bh_status build_tree(bh_ctx *ctx) {
   // clear per-build counters (interactions/fallbacks are per walk)
   prof_begin(ctx, &pp, 0);
   CK(launch_bbox(ctx->W, n, s));
-  CK(launch_keys(ctx->W, n, s));
-  prof_end(ctx, &pp, 3);
+  prof_end(ctx, &pp, 1);
+  // K1 + K2: the near-sorted path from the previous build's order, else (its
+  // device flag cleared) K1 and the full radix sort
   prof_begin(ctx, &pp, 1);
   int buf = 0;
+  if (ctx->near_sort) CK(launch_near_sort(ctx->W, n, s));
+  CK(launch_keys(ctx->W, n, s));
   CK(launch_sort(ctx->W, n, s, &buf));
   CK(launch_tie_fixup(ctx->W, n, buf, s));
-  prof_end(ctx, &pp, SORT_PASSES + 1);
+  prof_end(ctx, &pp, (ctx->near_sort ? 22 : 0) + 2 + SORT_PASSES + 1);
   ctx->sort_buf = buf;
   prof_begin(ctx, &pp, 2);
   CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, s));
@@ -514,6 +518,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->walked = false;
   ctx->walk_stats = 0;
   ctx->use_graphs = getenv("BH_NO_GRAPHS") ? 0 : 1;
+  ctx->near_sort = getenv("BH_NO_NEAR_SORT") ? 0 : 1;
   ctx->step_graph[0] = ctx->step_graph[1] = nullptr;
   ctx->sm_local = getenv("BH_SM_LOCAL") ? atoi(getenv("BH_SM_LOCAL")) : 0;
   ctx->num_sms = 148;
@@ -563,6 +568,9 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
       if (cudaMemsetAsync(ctx->W.vel4, 0, (size_t)own_n * 16, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
     }
     if (cudaMemsetAsync(ctx->W.icount, 0, (size_t)n * 4, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
+    // storage order is the step-0 Morton order: the previous order of the first
+    // build's near-sorted path is the identity (vals[0] always holds a permutation)
+    k_iota<<<blocks_for(n), 256, 0, s>>>(ctx->W.vals[0], n);
     if (cudaMemsetAsync(ctx->W.gcost, 0, ((size_t)n / 2 + 64) * 4, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
     st = do_sync(ctx);
   } while (0);
@@ -893,6 +901,8 @@ bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out) {
   out->opens = (int64_t)ctx->hstatus->opens;
   out->lane_iters = (int64_t)ctx->hstatus->iters;
   out->redo_targets = (int64_t)ctx->hstatus->n_redo;
+  out->near_sorted = ctx->hstatus->near_ok ? 1 : 0;
+  out->sort_bad_keys = ctx->hstatus->n_bad;
   out->interactions_cum = (int64_t)ctx->hstatus->interactions_cum;
   out->opens_cum = (int64_t)ctx->hstatus->opens_cum;
   out->own_begin = ctx->own_lo;

@@ -59,6 +59,8 @@ struct DevStatus {
   unsigned long long n_redo;         // last walk: targets re-walked with the exact fp64 MAC
   unsigned long long walk_next;      // last walk: next target group of the persistent lane walk
   uint32_t sm_next[256];             // walk: next chunk of each SM's segment (zeroed per walk)
+  uint32_t near_ok;     // this build's sort came from the near-sorted path (sort.cu)
+  uint32_t n_bad;       // near-sorted path: keys out of local order, sorted apart
   unsigned long long interactions_cum;  // since create / set_state
   unsigned long long opens_cum;
   float lo[3];
@@ -148,7 +150,10 @@ void bind_workspace(const Layout &L, void *base, Workspace &W);
 // ---- kernel launchers (each returns cudaGetLastError()) -------------------
 cudaError_t launch_bbox(const Workspace &W, int64_t n, cudaStream_t s);
 cudaError_t launch_keys(const Workspace &W, int64_t n, cudaStream_t s);
+cudaError_t launch_keys_prev(const Workspace &W, int64_t n, cudaStream_t s);
 cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *final_buf);
+cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s);
+cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s);
 cudaError_t launch_tie_fixup(const Workspace &W, int64_t n, int buf, cudaStream_t s);
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, cudaStream_t s);
 cudaError_t launch_moments(const Workspace &W, int64_t n, int64_t cap_rec, int64_t cap_int, double theta,

@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256) k_keys(const float4 *__restrict__ pos4, i
                                               const DevStatus *__restrict__ st,
                                               unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
                                               uint32_t *__restrict__ hist) {
+  if (st->near_ok) return;  // this build's near-sorted path already sorted the keys
   __shared__ uint32_t sh[SORT_PASSES][SORT_RADIX];
   for (int i = threadIdx.x; i < SORT_PASSES * SORT_RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
@@ -171,6 +172,31 @@ cudaError_t launch_bbox(const Workspace &W, int64_t n, cudaStream_t s) {
   int grid = (int)(need < BBOX_BLOCKS ? need : BBOX_BLOCKS);
   if (grid < 1) grid = 1;
   k_bbox<<<grid, 256, 0, s>>>(W.pos4, n, W.bbox_part, W.status);
+  return cudaGetLastError();
+}
+
+// K1 of the near-sorted path: the keys in the previous build's sorted order
+// (vals[0] holds it: sorted position -> storage id), written in place into
+// keys[0]; vals[0] is left as it is.  Switches the near-sorted path on.
+__global__ void __launch_bounds__(256) k_keys_prev(const float4 *__restrict__ pos4, int64_t n, DevStatus *st,
+                                                   unsigned long long *__restrict__ keys,
+                                                   const uint32_t *__restrict__ vals) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->near_ok = 1u;
+    st->n_bad = 0u;
+  }
+  const float lo0 = st->lo[0], lo1 = st->lo[1], lo2 = st->lo[2], sc = st->scale;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const float4 q = __ldg(&pos4[vals[p]]);
+    keys[p] = spread3(quantise(q.x, lo0, sc)) << 2 | spread3(quantise(q.y, lo1, sc)) << 1 | spread3(quantise(q.z, lo2, sc));
+  }
+}
+
+cudaError_t launch_keys_prev(const Workspace &W, int64_t n, cudaStream_t s) {
+  int64_t need = (n + 255) / 256;
+  int grid = (int)(need < 148 * 16 ? need : 148 * 16);
+  if (grid < 1) grid = 1;
+  k_keys_prev<<<grid, 256, 0, s>>>(W.pos4, n, W.status, W.keys[0], W.vals[0]);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,202 @@
+// nearsort.cu -- K2 fast path: sorting keys that are nearly in order.
+//
+// Reading L13 fixes the result: keys ascending, ties by user
+// index.  Between two steps particles move by v dt, so the keys listed in the
+// previous build's sorted order are almost sorted already (2^22 Plummer,
+// dt = 1e-4: 0.45 % descents; 1.7 % of the keys are out of order w.r.t. their
+// 4 neighbours on either side; a few jump far, across coarse cells).  The path:
+//   K1'  k_keys_prev   keys in the previous order (keys.cu), in place in keys[0]
+//   k_near_mark        flag a key "bad" if one of the NS_W keys before it is
+//                      larger or one of the NS_W keys after it is smaller
+//   scan of the flags  (scan.cu)
+//   k_near_check       the bad keys must fit the capacity of the next stage
+//   k_near_split       bad keys -> keys[1][0 .. nb), good keys -> keys[1][nb .. n)
+//                      (both in sequence order) + the bad keys' digit histograms
+//   k_onesweep x 8     radix sort of the bad keys only (sort.cu, SORT_BAD)
+//   k_near_merge       merge by rank: good i -> i + #{bad < k}, bad j ->
+//                      j + #{good <= k}; good keys found out of order switch the
+//                      path off
+// Every kernel after K1' runs only while st->near_ok is set; when it is cleared
+// (too many bad keys, or the good keys are not sorted) the full radix sort of
+// sort.cu runs instead (its kernels run only when near_ok is clear), so the
+// result is always the full sort's.  Equal keys end in some order and
+// k_tie_fixup re-sorts them by user index, as on the full path.
+// HBM: K1' 32 B, mark 8 B, split 24 B, merge 24 B per key (+ the bad keys'
+// passes), against 32 + 192 B per key for K1 + the 8 full passes.
+#include "bh_internal.cuh"
+
+namespace bh {
+
+constexpr int NS_BLOCK = 256;
+constexpr int NS_ITEMS = 8;
+constexpr int NS_TILE = NS_BLOCK * NS_ITEMS;
+constexpr int NS_W = 4;           // local-order window
+constexpr int NM_SMEM = 2048;     // bad keys a merge tile stages in shared memory
+
+__global__ void __launch_bounds__(NS_BLOCK) k_near_mark(const unsigned long long *__restrict__ keys, int64_t n,
+                                                        uint32_t *__restrict__ flags) {
+  __shared__ unsigned long long sk[NS_TILE + 2 * NS_W];
+  const int64_t t0 = blockIdx.x * (int64_t)NS_TILE;
+  for (int i = threadIdx.x; i < NS_TILE + 2 * NS_W; i += NS_BLOCK) {
+    const int64_t p = t0 - NS_W + i;
+    sk[i] = p < 0 ? 0ull : (p >= n ? ~0ull : keys[p]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NS_ITEMS; j++) {
+    const int i = j * NS_BLOCK + threadIdx.x;
+    const int64_t p = t0 + i;
+    if (p < n) {
+      const unsigned long long k = sk[i + NS_W];
+      bool bad = false;
+#pragma unroll
+      for (int d = 1; d <= NS_W; d++) bad |= (sk[i + NS_W - d] > k) | (sk[i + NS_W + d] < k);
+      flags[p] = bad ? 1u : 0u;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) flags[n] = 0u;
+}
+
+__global__ void k_near_check(const uint32_t *__restrict__ scan, int64_t n, int64_t cap_bad, DevStatus *st) {
+  if (!st->near_ok) return;
+  const uint32_t nb = scan[n];
+  st->n_bad = nb;
+  if ((int64_t)nb > cap_bad) st->near_ok = 0u;
+}
+
+__global__ void __launch_bounds__(256) k_near_split(const unsigned long long *__restrict__ keys0,
+                                                    const uint32_t *__restrict__ vals0,
+                                                    const uint32_t *__restrict__ scan, int64_t n,
+                                                    unsigned long long *__restrict__ keys1,
+                                                    uint32_t *__restrict__ vals1, uint32_t *__restrict__ hist,
+                                                    const DevStatus *__restrict__ st) {
+  if (!st->near_ok) return;
+  __shared__ uint32_t sh[SORT_PASSES][SORT_RADIX];
+  for (int i = threadIdx.x; i < SORT_PASSES * SORT_RADIX; i += blockDim.x) (&sh[0][0])[i] = 0u;
+  __syncthreads();
+  const int64_t nb = st->n_bad;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys0[p];
+    const uint32_t v = vals0[p];
+    const uint32_t e = scan[p];
+    if (scan[p + 1] != e) {  // bad
+      keys1[e] = k;
+      vals1[e] = v;
+#pragma unroll
+      for (int d = 0; d < SORT_PASSES; d++) atomicAdd(&sh[d][(uint32_t)(k >> (8 * d)) & 0xffu], 1u);
+    } else {
+      const int64_t q = nb + (p - (int64_t)e);
+      keys1[q] = k;
+      vals1[q] = v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < SORT_PASSES * SORT_RADIX; i += blockDim.x) {
+    const uint32_t c = (&sh[0][0])[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+// first index in a[lo, hi) with a[i] >= k (lower) or a[i] > k (upper)
+__device__ __forceinline__ int64_t bsearch_lb(const unsigned long long *__restrict__ a, int64_t lo, int64_t hi,
+                                              unsigned long long k, bool upper) {
+  while (lo < hi) {
+    const int64_t mid = lo + ((hi - lo) >> 1);
+    const unsigned long long x = a[mid];
+    if (upper ? x <= k : x < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long long *__restrict__ keys1,
+                                                         const uint32_t *__restrict__ vals1, int64_t n,
+                                                         unsigned long long *__restrict__ keys0,
+                                                         uint32_t *__restrict__ vals0, DevStatus *st) {
+  if (!st->near_ok) return;
+  __shared__ unsigned long long sbad[NM_SMEM];
+  __shared__ int64_t s_lo, s_hi;
+  const int64_t nb = st->n_bad, ng = n - nb;
+  const unsigned long long *bad = keys1;
+  const unsigned long long *good = keys1 + nb;
+  const int64_t gtiles = (ng + NS_TILE - 1) / NS_TILE;
+  const int64_t btiles = (nb + NS_TILE - 1) / NS_TILE;
+  bool unsorted = false;
+  for (int64_t t = blockIdx.x; t < gtiles + btiles; t += gridDim.x) {
+    if (t < gtiles) {
+      // good keys: their bad-key counts lie in [lb(first), lb(last)]
+      const int64_t g0 = t * NS_TILE, g1 = g0 + NS_TILE < ng ? g0 + NS_TILE : ng;
+      if (threadIdx.x == 0) {
+        s_lo = bsearch_lb(bad, 0, nb, good[g0], false);
+        s_hi = bsearch_lb(bad, s_lo, nb, good[g1 - 1], false);
+      }
+      __syncthreads();
+      const int64_t lo = s_lo, hi = s_hi;
+      const bool staged = hi - lo <= NM_SMEM;
+      if (staged)
+        for (int64_t i = threadIdx.x; i < hi - lo; i += NS_BLOCK) sbad[i] = bad[lo + i];
+      __syncthreads();
+      for (int64_t i = g0 + threadIdx.x; i < g1; i += NS_BLOCK) {
+        const unsigned long long k = good[i];
+        if (i + 1 < ng && good[i + 1] < k) unsorted = true;
+        int64_t c;
+        if (staged) {
+          int64_t a = 0, b = hi - lo;
+          while (a < b) {
+            const int64_t mid = (a + b) >> 1;
+            if (sbad[mid] < k) a = mid + 1;
+            else b = mid;
+          }
+          c = lo + a;
+        } else {
+          c = bsearch_lb(bad, lo, hi, k, false);
+        }
+        const int64_t pos = i + c;
+        keys0[pos] = k;
+        vals0[pos] = vals1[nb + i];
+      }
+      __syncthreads();
+    } else {
+      // bad keys (sorted by the radix passes): rank among the good keys
+      const int64_t j0 = (t - gtiles) * NS_TILE;
+      for (int64_t j = j0 + threadIdx.x; j < j0 + NS_TILE && j < nb; j += NS_BLOCK) {
+        const unsigned long long k = bad[j];
+        const int64_t pos = j + bsearch_lb(good, 0, ng, k, true);
+        keys0[pos] = k;
+        vals0[pos] = vals1[j];
+      }
+    }
+  }
+  if (unsorted) st->near_ok = 0u;
+}
+
+cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s) {
+  if (n < 1) return cudaSuccess;
+  cudaError_t e = launch_keys_prev(W, n, s);
+  if (e != cudaSuccess) return e;
+  const unsigned tiles = (unsigned)((n + NS_TILE - 1) / NS_TILE);
+  k_near_mark<<<tiles, NS_BLOCK, 0, s>>>(W.keys[0], n, W.nstart);
+  e = launch_scan_u32(W.nstart, n + 1, W.scan_tmp, s);
+  if (e != cudaSuccess) return e;
+  // capacity of the bad-key sort: its tiles' look-back status must fit the
+  // full sort's status area
+  int64_t cap_bad = n / 8 > SORT_TILE ? n / 8 : SORT_TILE;
+  const int64_t btiles = (cap_bad + SORT_TILE - 1) / SORT_TILE;
+  k_near_check<<<1, 1, 0, s>>>(W.nstart, n, cap_bad, W.status);
+  // zero the bad keys' histograms, tile tickets and look-back status
+  e = cudaMemsetAsync(W.sort_hist, 0,
+                      sizeof(uint32_t) * (SORT_PASSES * SORT_RADIX + 8 + (size_t)SORT_PASSES * btiles * SORT_RADIX), s);
+  if (e != cudaSuccess) return e;
+  int64_t sg = (n + 255) / 256;
+  if (sg > 148 * 8) sg = 148 * 8;
+  k_near_split<<<(unsigned)sg, 256, 0, s>>>(W.keys[0], W.vals[0], W.nstart, n, W.keys[1], W.vals[1], W.sort_hist,
+                                            W.status);
+  e = launch_sort_bad(W, btiles, s);
+  if (e != cudaSuccess) return e;
+  int64_t mg = (n + NS_TILE - 1) / NS_TILE + 1;
+  if (mg > 148 * 8) mg = 148 * 8;
+  k_near_merge<<<(unsigned)mg, NS_BLOCK, 0, s>>>(W.keys[1], W.vals[1], n, W.keys[0], W.vals[0], W.status);
+  return cudaGetLastError();
+}
+
+}  // namespace bh

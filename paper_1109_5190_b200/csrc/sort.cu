@@ -93,20 +93,30 @@ __device__ __forceinline__ uint32_t match8(uint32_t act, uint32_t dig) {
   return peers;
 }
 
+// mode: SORT_FULL runs unless this build's near-sorted path succeeded
+// (st->near_ok); SORT_BAD sorts the near-sorted path's st->n_bad out-of-order
+// keys and runs only if that path is still on.
+enum { SORT_FULL = 0, SORT_BAD = 1 };
+
 __global__ void __launch_bounds__(SORT_BLOCK, 2) k_onesweep(const unsigned long long *__restrict__ kin,
                                                          const uint32_t *__restrict__ vin,
                                                          unsigned long long *__restrict__ kout,
-                                                         uint32_t *__restrict__ vout, int64_t n, int shift,
+                                                         uint32_t *__restrict__ vout, int64_t n_arg, int shift,
                                                          const uint32_t *__restrict__ hist, uint32_t *status,
-                                                         uint32_t *tile_ctr) {
+                                                         uint32_t *tile_ctr, const DevStatus *__restrict__ st,
+                                                         int mode) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem &S = *reinterpret_cast<SortSmem *>(smem_raw);
+  const uint32_t near = st->near_ok;
+  if (mode == SORT_FULL ? near != 0u : near == 0u) return;  // uniform
+  const int64_t n = mode == SORT_FULL ? n_arg : (int64_t)st->n_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
   for (int i = tid; i < SORT_WARPS * SORT_RADIX; i += SORT_BLOCK) (&S.wcount[0][0])[i] = 0;
   __syncthreads();
   const uint32_t tile = S.tile;
   const int64_t tbase = (int64_t)tile * SORT_TILE;
+  if (tbase >= n && tile > 0) return;  // past the data (SORT_BAD sizes its grid for the capacity)
   const int64_t wbase = tbase + (int64_t)warp * 32 * SORT_ITEMS;
 
   unsigned long long k[SORT_ITEMS];
@@ -243,10 +253,30 @@ cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *fina
   for (int pass = 0; pass < SORT_PASSES; pass++) {
     k_onesweep<<<(unsigned)tiles, SORT_BLOCK, sizeof(SortSmem), s>>>(
         W.keys[src], pass == 0 ? nullptr : W.vals[src], W.keys[src ^ 1], W.vals[src ^ 1], n, 8 * pass, W.sort_hist + pass * SORT_RADIX,
-        W.sort_status + (size_t)pass * tiles * SORT_RADIX, W.sort_tilectr + pass);
+        W.sort_status + (size_t)pass * tiles * SORT_RADIX, W.sort_tilectr + pass, W.status, SORT_FULL);
     src ^= 1;
   }
   *final_buf = src;
+  return cudaGetLastError();
+}
+
+// the near-sorted path's bad keys: keys[1][0 .. st->n_bad) with their ids, 8
+// passes through keys[0] and back (the count lives on the device; the grid is
+// sized for the capacity, tiles past the data return at once)
+cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int src = 1;
+  for (int pass = 0; pass < SORT_PASSES; pass++) {
+    k_onesweep<<<(unsigned)tiles, SORT_BLOCK, sizeof(SortSmem), s>>>(
+        W.keys[src], W.vals[src], W.keys[src ^ 1], W.vals[src ^ 1], 0, 8 * pass, W.sort_hist + pass * SORT_RADIX,
+        W.sort_status + (size_t)pass * tiles * SORT_RADIX, W.sort_tilectr + pass, W.status, SORT_BAD);
+    src ^= 1;
+  }
   return cudaGetLastError();
 }
 

@@ -347,3 +347,40 @@ def test_resume_rare_paths(BH, monkeypatch, hook):
     check_step0(bh, o, m.shape[0])
     st = bh.get_stats()
     assert st["redo_targets"] > 4, "the input must exercise the resume path"
+
+
+def test_near_sorted_path_matches_full_sort(BH, monkeypatch):
+    """The near-sorted sort (keys in the previous build's order, out-of-order
+    keys sorted apart and merged) gives bitwise the full radix sort's keys,
+    permutation and trajectory, and falls back to the full sort when the
+    order is lost (positions permuted by set_state)."""
+    m, p, v = bhgen.generate("cfg2", n=50000)
+    prm = bhgen.params("cfg2")
+    a = BH(m, p, v, **prm)
+    monkeypatch.setenv("BH_NO_NEAR_SORT", "1")
+    b = BH(m, p, v, **prm)
+    monkeypatch.delenv("BH_NO_NEAR_SORT")
+    for _ in range(3):
+        a.step(1)
+        b.step(1)
+        a.build_tree()
+        b.build_tree()
+        ka, pa = a.get_keys()
+        kb, pb = b.get_keys()
+        assert np.array_equal(ka, kb) and np.array_equal(pa, pb)
+        assert a.get_stats()["near_sorted"] == 1 and b.get_stats()["near_sorted"] == 0
+    assert np.array_equal(a.get_state()[0], b.get_state()[0])
+    # a scrambled state: the previous order is useless -> full sort, same result
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(m.shape[0])
+    a.set_state(m, p[perm], v[perm])
+    b.set_state(m, p[perm], v[perm])
+    a.build_tree()
+    b.build_tree()
+    assert a.get_stats()["near_sorted"] == 0
+    ka, pa = a.get_keys()
+    kb, pb = b.get_keys()
+    assert np.array_equal(ka, kb) and np.array_equal(pa, pb)
+    o = _oracle(m, p[perm], v[perm], prm)
+    ok, operm = o.keys()
+    assert np.array_equal(ka, ok) and np.array_equal(pa.astype(np.int64), operm)
