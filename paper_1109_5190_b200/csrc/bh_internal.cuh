@@ -150,7 +150,7 @@ void bind_workspace(const Layout &L, void *base, Workspace &W);
 // ---- kernel launchers (each returns cudaGetLastError()) -------------------
 cudaError_t launch_bbox(const Workspace &W, int64_t n, cudaStream_t s);
 cudaError_t launch_keys(const Workspace &W, int64_t n, cudaStream_t s);
-cudaError_t launch_keys_prev(const Workspace &W, int64_t n, cudaStream_t s);
+cudaError_t launch_keys_prev(const Workspace &W, int64_t n, uint32_t *flags, cudaStream_t s);
 cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *final_buf);
 cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s);
 cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s);

@@ -175,28 +175,53 @@ cudaError_t launch_bbox(const Workspace &W, int64_t n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// K1 of the near-sorted path: the keys in the previous build's sorted order
-// (vals[0] holds it: sorted position -> storage id), written in place into
-// keys[0]; vals[0] is left as it is.  Switches the near-sorted path on.
+// K1 of the near-sorted path (nearsort.cu): the keys in the previous build's
+// sorted order (vals[0]: sorted position -> storage id), written in place into
+// keys[0] (vals[0] is left as it is), and the local-order flags: flags[p] = 1
+// if one of the NS_W keys before p is larger or one of the NS_W keys after it
+// is smaller (the halo keys are recomputed, not re-read).  Switches the path on.
+constexpr int KP_ITEMS = 8, KP_W = 4, KP_TILE = 256 * KP_ITEMS;
 __global__ void __launch_bounds__(256) k_keys_prev(const float4 *__restrict__ pos4, int64_t n, DevStatus *st,
                                                    unsigned long long *__restrict__ keys,
-                                                   const uint32_t *__restrict__ vals) {
+                                                   const uint32_t *__restrict__ vals, uint32_t *__restrict__ flags) {
+  __shared__ unsigned long long sk[KP_TILE + 2 * KP_W];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->near_ok = 1u;
     st->n_bad = 0u;
+    flags[n] = 0u;
   }
   const float lo0 = st->lo[0], lo1 = st->lo[1], lo2 = st->lo[2], sc = st->scale;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    const float4 q = __ldg(&pos4[vals[p]]);
-    keys[p] = spread3(quantise(q.x, lo0, sc)) << 2 | spread3(quantise(q.y, lo1, sc)) << 1 | spread3(quantise(q.z, lo2, sc));
+  const int64_t t0 = blockIdx.x * (int64_t)KP_TILE;
+  for (int i = threadIdx.x; i < KP_TILE + 2 * KP_W; i += 256) {
+    const int64_t p = t0 - KP_W + i;
+    unsigned long long k;
+    if (p < 0) k = 0ull;
+    else if (p >= n) k = ~0ull;
+    else {
+      const float4 q = __ldg(&pos4[vals[p]]);
+      k = spread3(quantise(q.x, lo0, sc)) << 2 | spread3(quantise(q.y, lo1, sc)) << 1 | spread3(quantise(q.z, lo2, sc));
+      if (i >= KP_W && i < KP_TILE + KP_W) keys[p] = k;
+    }
+    sk[i] = k;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < KP_ITEMS; j++) {
+    const int i = j * 256 + threadIdx.x;
+    const int64_t p = t0 + i;
+    if (p < n) {
+      const unsigned long long k = sk[i + KP_W];
+      bool bad = false;
+#pragma unroll
+      for (int d = 1; d <= KP_W; d++) bad |= (sk[i + KP_W - d] > k) | (sk[i + KP_W + d] < k);
+      flags[p] = bad ? 1u : 0u;
+    }
   }
 }
 
-cudaError_t launch_keys_prev(const Workspace &W, int64_t n, cudaStream_t s) {
-  int64_t need = (n + 255) / 256;
-  int grid = (int)(need < 148 * 16 ? need : 148 * 16);
-  if (grid < 1) grid = 1;
-  k_keys_prev<<<grid, 256, 0, s>>>(W.pos4, n, W.status, W.keys[0], W.vals[0]);
+cudaError_t launch_keys_prev(const Workspace &W, int64_t n, uint32_t *flags, cudaStream_t s) {
+  k_keys_prev<<<(unsigned)((n + KP_TILE - 1) / KP_TILE), 256, 0, s>>>(W.pos4, n, W.status, W.keys[0], W.vals[0],
+                                                                     flags);
   return cudaGetLastError();
 }
 

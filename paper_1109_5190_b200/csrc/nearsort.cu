@@ -5,14 +5,15 @@
 // previous build's sorted order are almost sorted already (2^22 Plummer,
 // dt = 1e-4: 0.45 % descents; 1.7 % of the keys are out of order w.r.t. their
 // 4 neighbours on either side; a few jump far, across coarse cells).  The path:
-//   K1'  k_keys_prev   keys in the previous order (keys.cu), in place in keys[0]
-//   k_near_mark        flag a key "bad" if one of the NS_W keys before it is
-//                      larger or one of the NS_W keys after it is smaller
+//   K1'  k_keys_prev   keys in the previous order (keys.cu), in place in keys[0],
+//                      and a "bad" flag per key: one of the 4 keys before it is
+//                      larger or one of the 4 keys after it is smaller
 //   scan of the flags  (scan.cu)
 //   k_near_check       the bad keys must fit the capacity of the next stage
 //   k_near_split       bad keys -> keys[1][0 .. nb), good keys -> keys[1][nb .. n)
 //                      (both in sequence order) + the bad keys' digit histograms
 //   k_onesweep x 8     radix sort of the bad keys only (sort.cu, SORT_BAD)
+//   k_near_tiles       per merge tile of good keys, the bad keys below its first
 //   k_near_merge       merge by rank: good i -> i + #{bad < k}, bad j ->
 //                      j + #{good <= k}; good keys found out of order switch the
 //                      path off
@@ -21,7 +22,7 @@
 // sort.cu runs instead (its kernels run only when near_ok is clear), so the
 // result is always the full sort's.  Equal keys end in some order and
 // k_tie_fixup re-sorts them by user index, as on the full path.
-// HBM: K1' 32 B, mark 8 B, split 24 B, merge 24 B per key (+ the bad keys'
+// HBM: K1' 32 B (+4 B flags), scan ~12 B, split 28 B, merge 24 B per key (+ the bad keys'
 // passes), against 32 + 192 B per key for K1 + the 8 full passes.
 #include "bh_internal.cuh"
 
@@ -30,32 +31,7 @@ namespace bh {
 constexpr int NS_BLOCK = 256;
 constexpr int NS_ITEMS = 8;
 constexpr int NS_TILE = NS_BLOCK * NS_ITEMS;
-constexpr int NS_W = 4;           // local-order window
 constexpr int NM_SMEM = 2048;     // bad keys a merge tile stages in shared memory
-
-__global__ void __launch_bounds__(NS_BLOCK) k_near_mark(const unsigned long long *__restrict__ keys, int64_t n,
-                                                        uint32_t *__restrict__ flags) {
-  __shared__ unsigned long long sk[NS_TILE + 2 * NS_W];
-  const int64_t t0 = blockIdx.x * (int64_t)NS_TILE;
-  for (int i = threadIdx.x; i < NS_TILE + 2 * NS_W; i += NS_BLOCK) {
-    const int64_t p = t0 - NS_W + i;
-    sk[i] = p < 0 ? 0ull : (p >= n ? ~0ull : keys[p]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < NS_ITEMS; j++) {
-    const int i = j * NS_BLOCK + threadIdx.x;
-    const int64_t p = t0 + i;
-    if (p < n) {
-      const unsigned long long k = sk[i + NS_W];
-      bool bad = false;
-#pragma unroll
-      for (int d = 1; d <= NS_W; d++) bad |= (sk[i + NS_W - d] > k) | (sk[i + NS_W + d] < k);
-      flags[p] = bad ? 1u : 0u;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) flags[n] = 0u;
-}
 
 __global__ void k_near_check(const uint32_t *__restrict__ scan, int64_t n, int64_t cap_bad, DevStatus *st) {
   if (!st->near_ok) return;
@@ -109,13 +85,25 @@ __device__ __forceinline__ int64_t bsearch_lb(const unsigned long long *__restri
   return lo;
 }
 
+// merge tiles: tlo[t] = #{bad < first good key of tile t}, tlo[gtiles] = nb
+// (one binary search per tile, all tiles in parallel)
+__global__ void k_near_tiles(const unsigned long long *__restrict__ keys1, int64_t n, uint32_t *__restrict__ tlo,
+                             const DevStatus *__restrict__ st) {
+  if (!st->near_ok) return;
+  const int64_t nb = st->n_bad, ng = n - nb;
+  const int64_t gtiles = (ng + NS_TILE - 1) / NS_TILE;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > gtiles) return;
+  tlo[t] = t == gtiles ? (uint32_t)nb : (uint32_t)bsearch_lb(keys1, 0, nb, keys1[nb + t * NS_TILE], false);
+}
+
 __global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long long *__restrict__ keys1,
                                                          const uint32_t *__restrict__ vals1, int64_t n,
                                                          unsigned long long *__restrict__ keys0,
-                                                         uint32_t *__restrict__ vals0, DevStatus *st) {
+                                                         uint32_t *__restrict__ vals0,
+                                                         const uint32_t *__restrict__ tlo, DevStatus *st) {
   if (!st->near_ok) return;
   __shared__ unsigned long long sbad[NM_SMEM];
-  __shared__ int64_t s_lo, s_hi;
   const int64_t nb = st->n_bad, ng = n - nb;
   const unsigned long long *bad = keys1;
   const unsigned long long *good = keys1 + nb;
@@ -126,12 +114,7 @@ __global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long lon
     if (t < gtiles) {
       // good keys: their bad-key counts lie in [lb(first), lb(last)]
       const int64_t g0 = t * NS_TILE, g1 = g0 + NS_TILE < ng ? g0 + NS_TILE : ng;
-      if (threadIdx.x == 0) {
-        s_lo = bsearch_lb(bad, 0, nb, good[g0], false);
-        s_hi = bsearch_lb(bad, s_lo, nb, good[g1 - 1], false);
-      }
-      __syncthreads();
-      const int64_t lo = s_lo, hi = s_hi;
+      const int64_t lo = tlo[t], hi = tlo[t + 1];  // sorted good keys: counts within [lo, hi]
       const bool staged = hi - lo <= NM_SMEM;
       if (staged)
         for (int64_t i = threadIdx.x; i < hi - lo; i += NS_BLOCK) sbad[i] = bad[lo + i];
@@ -172,10 +155,8 @@ __global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long lon
 
 cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s) {
   if (n < 1) return cudaSuccess;
-  cudaError_t e = launch_keys_prev(W, n, s);
+  cudaError_t e = launch_keys_prev(W, n, W.nstart, s);  // keys + local-order flags
   if (e != cudaSuccess) return e;
-  const unsigned tiles = (unsigned)((n + NS_TILE - 1) / NS_TILE);
-  k_near_mark<<<tiles, NS_BLOCK, 0, s>>>(W.keys[0], n, W.nstart);
   e = launch_scan_u32(W.nstart, n + 1, W.scan_tmp, s);
   if (e != cudaSuccess) return e;
   // capacity of the bad-key sort: its tiles' look-back status must fit the
@@ -195,7 +176,9 @@ cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   int64_t mg = (n + NS_TILE - 1) / NS_TILE + 1;
   if (mg > 148 * 8) mg = 148 * 8;
-  k_near_merge<<<(unsigned)mg, NS_BLOCK, 0, s>>>(W.keys[1], W.vals[1], n, W.keys[0], W.vals[0], W.status);
+  // merge-tile bounds go to nstart (free after the split; the tree build rewrites it)
+  k_near_tiles<<<(unsigned)((n / NS_TILE + 2 + 255) / 256), 256, 0, s>>>(W.keys[1], n, W.nstart, W.status);
+  k_near_merge<<<(unsigned)mg, NS_BLOCK, 0, s>>>(W.keys[1], W.vals[1], n, W.keys[0], W.vals[0], W.nstart, W.status);
   return cudaGetLastError();
 }
 
