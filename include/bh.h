@@ -77,8 +77,9 @@ typedef struct {
                               (n + max(n, min(21 n, 2^22)) + 64, which always fits
                               n <= 199,728 and typical inputs above that)              */
     int walk_group;     /* force-walk variant; every value gives bitwise-identical results:
-                           0 = default (packed fp32, 2 targets per lane, 4 lanes share one
-                           traversal: 8-target groups); 1, 2, 4, 8, 16, 32 = one target per
+                           0 = automatic: packed fp32, 2 targets per lane, 2 lanes share one
+                           traversal (4-target groups, code 68), or 4 lanes (8-target groups,
+                           code 67) when theta < 0.6 and n >= 2^22; 1, 2, 4, 8, 16, 32 = one target per
                            lane, that many lanes per traversal; 64..70 = packed variants
                            (64: 32 lanes x 2, 65/69/70: 8/4/2 lanes x 4, 66/67/68: 8/4/2 lanes x 2);
                            80..85 = persistent lane groups (80: 1 x 4, 81: 1 x 2, 82: 2 x 4,

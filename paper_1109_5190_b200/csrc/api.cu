@@ -379,7 +379,12 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   memset(&a, 0, sizeof a);
   a.n = n;
   a.buf = ctx->sort_buf;
-  a.group = ctx->p.walk_group;
+  // walk_group 0 = automatic: 4-target groups (2 lanes x 2 targets) unless the
+  // walks are long (theta < 0.6 on n >= 2^22: ~2000 interactions per target),
+  // where 8-target groups amortise the shared loads better (measured on the
+  // BASELINE configs)
+  a.group = ctx->p.walk_group != 0 ? ctx->p.walk_group
+                                   : ((ctx->p.theta < 0.6 && n >= ((int64_t)1 << 22)) ? 67 : 68);
   a.stats = ctx->walk_stats;
   a.sm_local = ctx->sm_local;
   a.num_sms = ctx->num_sms;
