@@ -97,59 +97,77 @@ __global__ void k_near_tiles(const unsigned long long *__restrict__ keys1, int64
   tlo[t] = t == gtiles ? (uint32_t)nb : (uint32_t)bsearch_lb(keys1, 0, nb, keys1[nb + t * NS_TILE], false);
 }
 
+// One block per tile of good keys.  The tile's good keys and the bad keys that
+// fall in its key range -- bad j in [tlo[t], tlo[t+1]), tile 0 also taking the
+// bad keys below every good key -- are staged in shared memory; good i goes to
+// i + #{bad < k}, bad j to j + #{good <= k}, both counted by binary search in
+// shared memory (global memory if a slice is larger than the stage).
 __global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long long *__restrict__ keys1,
                                                          const uint32_t *__restrict__ vals1, int64_t n,
                                                          unsigned long long *__restrict__ keys0,
                                                          uint32_t *__restrict__ vals0,
                                                          const uint32_t *__restrict__ tlo, DevStatus *st) {
   if (!st->near_ok) return;
-  __shared__ unsigned long long sbad[NM_SMEM];
+  __shared__ unsigned long long sbad[NM_SMEM], sgood[NS_TILE];
   const int64_t nb = st->n_bad, ng = n - nb;
   const unsigned long long *bad = keys1;
   const unsigned long long *good = keys1 + nb;
   const int64_t gtiles = (ng + NS_TILE - 1) / NS_TILE;
-  const int64_t btiles = (nb + NS_TILE - 1) / NS_TILE;
   bool unsorted = false;
-  for (int64_t t = blockIdx.x; t < gtiles + btiles; t += gridDim.x) {
-    if (t < gtiles) {
-      // good keys: their bad-key counts lie in [lb(first), lb(last)]
-      const int64_t g0 = t * NS_TILE, g1 = g0 + NS_TILE < ng ? g0 + NS_TILE : ng;
-      const int64_t lo = tlo[t], hi = tlo[t + 1];  // sorted good keys: counts within [lo, hi]
-      const bool staged = hi - lo <= NM_SMEM;
-      if (staged)
-        for (int64_t i = threadIdx.x; i < hi - lo; i += NS_BLOCK) sbad[i] = bad[lo + i];
-      __syncthreads();
-      for (int64_t i = g0 + threadIdx.x; i < g1; i += NS_BLOCK) {
-        const unsigned long long k = good[i];
-        if (i + 1 < ng && good[i + 1] < k) unsorted = true;
-        int64_t c;
-        if (staged) {
-          int64_t a = 0, b = hi - lo;
-          while (a < b) {
-            const int64_t mid = (a + b) >> 1;
-            if (sbad[mid] < k) a = mid + 1;
-            else b = mid;
-          }
-          c = lo + a;
-        } else {
-          c = bsearch_lb(bad, lo, hi, k, false);
+  for (int64_t t = blockIdx.x; t < gtiles; t += gridDim.x) {
+    const int64_t g0 = t * NS_TILE, g1 = g0 + NS_TILE < ng ? g0 + NS_TILE : ng, gn = g1 - g0;
+    const int64_t lo = tlo[t], hi = tlo[t + 1];      // bad keys with good[g0] <= k < good[g1]
+    const int64_t blo = t == 0 ? 0 : lo;             // tile 0 also takes the bad keys below good[0]
+    const bool staged = hi - lo <= NM_SMEM && hi >= lo;
+    for (int64_t i = threadIdx.x; i < gn; i += NS_BLOCK) sgood[i] = good[g0 + i];
+    if (staged)
+      for (int64_t i = threadIdx.x; i < hi - lo; i += NS_BLOCK) sbad[i] = bad[lo + i];
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < gn; i += NS_BLOCK) {
+      const unsigned long long k = sgood[i];
+      if ((i + 1 < gn ? sgood[i + 1] : (g1 < ng ? good[g1] : ~0ull)) < k) unsorted = true;
+      int64_t c;
+      if (staged) {
+        int64_t a = 0, b = hi - lo;
+        while (a < b) {
+          const int64_t mid = (a + b) >> 1;
+          if (sbad[mid] < k) a = mid + 1;
+          else b = mid;
         }
-        const int64_t pos = i + c;
-        keys0[pos] = k;
-        vals0[pos] = vals1[nb + i];
+        c = lo + a;
+      } else {
+        c = bsearch_lb(bad, 0, nb, k, false);
       }
-      __syncthreads();
-    } else {
-      // bad keys (sorted by the radix passes): rank among the good keys
-      const int64_t j0 = (t - gtiles) * NS_TILE;
-      for (int64_t j = j0 + threadIdx.x; j < j0 + NS_TILE && j < nb; j += NS_BLOCK) {
-        const unsigned long long k = bad[j];
-        const int64_t pos = j + bsearch_lb(good, 0, ng, k, true);
-        keys0[pos] = k;
-        vals0[pos] = vals1[j];
-      }
+      const int64_t pos = g0 + i + c;
+      keys0[pos] = k;
+      vals0[pos] = vals1[nb + g0 + i];
     }
+    for (int64_t j = blo + threadIdx.x; j < hi; j += NS_BLOCK) {
+      const unsigned long long k = (staged && j >= lo) ? sbad[j - lo] : bad[j];
+      int64_t c;
+      if (j < lo) {
+        c = 0;  // below every good key (tile 0 only)
+      } else {
+        int64_t a = 0, b = gn;  // #good <= k within this tile (k >= good[g0])
+        while (a < b) {
+          const int64_t mid = (a + b) >> 1;
+          if (sgood[mid] <= k) a = mid + 1;
+          else b = mid;
+        }
+        c = g0 + a;
+      }
+      const int64_t pos = j + c;
+      keys0[pos] = k;
+      vals0[pos] = vals1[j];
+    }
+    __syncthreads();
   }
+  // no good keys at all: the bad keys are the whole (sorted) sequence
+  if (gtiles == 0)
+    for (int64_t j = blockIdx.x * (int64_t)NS_BLOCK + threadIdx.x; j < nb; j += (int64_t)gridDim.x * NS_BLOCK) {
+      keys0[j] = bad[j];
+      vals0[j] = vals1[j];
+    }
   if (unsorted) st->near_ok = 0u;
 }
 
@@ -174,8 +192,7 @@ cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s) {
                                             W.status);
   e = launch_sort_bad(W, btiles, s);
   if (e != cudaSuccess) return e;
-  int64_t mg = (n + NS_TILE - 1) / NS_TILE + 1;
-  if (mg > 148 * 8) mg = 148 * 8;
+  int64_t mg = (n + NS_TILE - 1) / NS_TILE + 1;  // one block per good tile
   // merge-tile bounds go to nstart (free after the split; the tree build rewrites it)
   k_near_tiles<<<(unsigned)((n / NS_TILE + 2 + 255) / 256), 256, 0, s>>>(W.keys[1], n, W.nstart, W.status);
   k_near_merge<<<(unsigned)mg, NS_BLOCK, 0, s>>>(W.keys[1], W.vals[1], n, W.keys[0], W.vals[0], W.nstart, W.status);
