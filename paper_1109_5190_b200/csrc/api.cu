@@ -37,7 +37,6 @@ struct bh_ctx {
   bool tree_valid;
   bool walked;
   int walk_stats;
-  int sm_local;
   int use_graphs;
   cudaGraphExec_t step_graph[2];  // [0]: half kick (first step), [1]: full kick
   int num_sms;
@@ -386,7 +385,6 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.group = ctx->p.walk_group != 0 ? ctx->p.walk_group
                                    : ((ctx->p.theta < 0.6 && n >= ((int64_t)1 << 22)) ? 67 : 68);
   a.stats = ctx->walk_stats;
-  a.sm_local = ctx->sm_local;
   a.num_sms = ctx->num_sms;
   // containment test elision (see walk.cu): a cell holding the target has
   // s/d >= 1/sqrt(3) (d <= sqrt(3) s), so it never passes s/d < theta for
@@ -525,7 +523,6 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->use_graphs = getenv("BH_NO_GRAPHS") ? 0 : 1;
   ctx->near_sort = getenv("BH_NO_NEAR_SORT") ? 0 : 1;
   ctx->step_graph[0] = ctx->step_graph[1] = nullptr;
-  ctx->sm_local = getenv("BH_SM_LOCAL") ? atoi(getenv("BH_SM_LOCAL")) : 0;
   ctx->num_sms = 148;
   ctx->sort_buf = 0;
   ctx->status_pending = false;

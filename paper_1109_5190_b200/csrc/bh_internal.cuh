@@ -169,7 +169,6 @@ struct WalkArgs {
   int buf;              // sort buffer holding vals
   int group;            // lanes per shared traversal
   int stats;            // 1: also count opened nodes and SIMD slots
-  int sm_local;         // 1: SM-local chunk scheduling of the walk (see walk.cu)
   int num_sms;
   int need_cont;        // 0: theta < 1/sqrt(3) and eps > 0 -> no cell containing the
                         //    target can pass the MAC and the self record adds 0

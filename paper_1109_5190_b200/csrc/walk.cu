@@ -67,8 +67,7 @@ struct WalkParams {
   float eps2, G, kick, dt;
   double theta2;
   uint32_t own_lo;
-  int sm_local, num_sms;
-  uint32_t n_chunks;  // walk: chunks of 2 NP x 256 targets
+  int num_sms;
 };
 
 __device__ __forceinline__ float rsqrt_fast(float x) {
@@ -372,31 +371,7 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
   const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
   if (P.st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t Wn = P.st->n_records;
-  // SM-local scheduling: the chunks (one block's targets) are split into one
-  // contiguous Morton segment per SM; a block takes the next chunk of its SM's
-  // segment (so the blocks resident on an SM walk neighbouring regions and share
-  // L1), or steals from the following segments once its own is done.  Every
-  // block claims exactly one chunk and there are as many blocks as chunks.
-  uint32_t chunk = blockIdx.x;
-  if (P.sm_local) {
-    __shared__ uint32_t s_chunk;
-    if (threadIdx.x == 0) {
-      uint32_t sm;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-      const uint32_t ns = (uint32_t)P.num_sms;
-      sm %= ns;
-      for (uint32_t k = 0;; k++) {
-        const uint32_t seg = (sm + k) % ns;
-        const uint32_t lo = (uint32_t)((unsigned long long)P.n_chunks * seg / ns);
-        const uint32_t hi = (uint32_t)((unsigned long long)P.n_chunks * (seg + 1) / ns);
-        if (lo == hi) continue;
-        const uint32_t got = atomicAdd(&P.st->sm_next[seg], 1u);
-        if (lo + got < hi) { s_chunk = lo + got; break; }
-      }
-    }
-    __syncthreads();
-    chunk = s_chunk;
-  }
+  const uint32_t chunk = blockIdx.x;
   // Group order.  The block's 256 / GL groups are dealt to its warps in
   // descending order of their last-walk cost (union-walk iterations, gcost):
   // a warp runs until its slowest group is done, so warps of similar groups
@@ -756,7 +731,13 @@ __global__ void __launch_bounds__(256, (NP == 1 || !PERSIST) ? 4 : 3) k_walk_lan
 // bounded by ~2 x 32 x depth) hands the remaining segments to lane 0, which
 // walks each one stacklessly.
 constexpr int RESUME_WARPS = 4;
-constexpr int RESUME_STACK = 1024;
+#ifndef BH_RESUME_STACK_N
+#define BH_RESUME_STACK_N 512
+#endif
+#ifndef BH_RESUME_MINB
+#define BH_RESUME_MINB 8
+#endif
+constexpr int RESUME_STACK = BH_RESUME_STACK_N;
 
 struct ResumeAcc {
   double ax, ay, az;
@@ -790,7 +771,7 @@ __device__ __forceinline__ bool resume_visit(const WalkParams &P, const Target &
   return acc;
 }
 
-__global__ void __launch_bounds__(32 * RESUME_WARPS) k_walk_resume(const WalkParams P) {
+__global__ void __launch_bounds__(32 * RESUME_WARPS, BH_RESUME_MINB) k_walk_resume(const WalkParams P) {
   __shared__ uint2 stack[RESUME_WARPS][RESUME_STACK];
   if (P.st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t full = 0xffffffffu;
@@ -914,9 +895,8 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.dt = a.dt;
   P.theta2 = a.theta2;
   P.own_lo = a.own_lo;
-  P.sm_local = a.sm_local;
   P.num_sms = a.num_sms > 0 ? a.num_sms : 148;
-  if (P.sm_local || (!a.stats && a.group >= 80 && a.group <= 95)) {
+  if (!a.stats && a.group >= 80 && a.group <= 95) {
     cudaError_t e = cudaMemsetAsync(W.status->sm_next, 0, sizeof(W.status->sm_next), s);
     if (e != cudaSuccess) return e;
   }
@@ -981,7 +961,6 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
     const bool cont = a.need_cont;
     if (a.group >= 66 && a.group <= 68) {  // 8 / 4 / 2 lanes x 2 targets (16-, 8-, 4-target groups)
       const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
-      P.n_chunks = grid2;
       if (a.group == 66) {
         if (cont) k_walk2<8, 1, true><<<grid2, 256, 0, s>>>(P);
         else k_walk2<8, 1, false><<<grid2, 256, 0, s>>>(P);
@@ -994,7 +973,6 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
       }
     } else if (a.group == 65 || a.group == 69 || a.group == 70) {  // 4 targets per lane
       const unsigned g4 = (unsigned)((a.n_targets + 1023) / 1024);
-      P.n_chunks = g4;
       if (a.group == 65) {
         if (cont) k_walk2<8, 2, true><<<g4, 256, 0, s>>>(P);
         else k_walk2<8, 2, false><<<g4, 256, 0, s>>>(P);
@@ -1007,7 +985,6 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
       }
     } else {
       const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
-      P.n_chunks = grid2;
       if (a.group == 64) {
         if (cont) k_walk2<32, 1, true><<<grid2, 256, 0, s>>>(P);
         else k_walk2<32, 1, false><<<grid2, 256, 0, s>>>(P);
@@ -1036,7 +1013,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   // the continuation of dropped-out targets: a fixed grid, grid-stride over the
   // device-side queue (lanes dense in queue order)
   int64_t eg = (a.n_targets + RESUME_WARPS - 1) / RESUME_WARPS;
-  if (eg > 148 * 8) eg = 148 * 8;
+  if (eg > 148 * 16) eg = 148 * 16;
   k_walk_resume<<<(unsigned)eg, 32 * RESUME_WARPS, 0, s>>>(P);
   return cudaGetLastError();
 }
