@@ -355,6 +355,9 @@ __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, floa
       : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip), "r"(drop));
 }
 
+#ifndef BH_WALK2_BLOCK
+#define BH_WALK2_BLOCK 128
+#endif
 #ifndef BH_WALK2_UNROLL
 #define BH_WALK2_UNROLL 2
 #endif
@@ -364,7 +367,7 @@ __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, floa
 // NP pairs of targets per lane (2 NP targets), GL lanes per group: a group of
 // 2 NP GL Morton-consecutive targets shares one traversal.
 template <int GL, int NP, bool CONT>
-__global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(const WalkParams P) {
+__global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 ? BH_WALK2_MINB : 4) * 256 / BH_WALK2_BLOCK) k_walk2(const WalkParams P) {
   constexpr int TPL = 2 * NP;  // targets per lane
   const uint32_t full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(256, NP == 1 ? BH_WALK2_MINB : 4) k_walk2(cons
   // a warp runs until its slowest group is done, so warps of similar groups
   // idle less (the groups themselves -- which targets walk together -- do not
   // change, hence neither do the results).  Without costs: Morton order.
-  constexpr int GPB = 256 / GL;  // groups per block
+  constexpr int GPB = BH_WALK2_BLOCK / GL;  // groups per block
   const int gi = lane / GL, gl = lane % GL;
   int lg = (threadIdx.x >> 5) * (32 / GL) + gi;  // local group of this lane
   if (P.gcost) {
@@ -953,46 +956,26 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
     }
 #undef BH_LANE_LAUNCH
   } else if (!a.stats && (a.group == 0 || a.group >= 64)) {
-    // production path: packed fp32 pairs of targets per lane
-    //   0 : 4 lanes x 2 targets (8-target groups)   [default]
-    //   64: 32 lanes x 2 targets (64-target groups)
-    //   65 / 69 / 70: 8 / 4 / 2 lanes x 4 targets
-    //   66 / 67 / 68: 8 / 4 / 2 lanes x 2 targets
+    // production path (k_walk2): packed fp32, lanes per group x targets per lane
+    //   66 / 67 / 68: 8 / 4 / 2 lanes x 2 targets   (api.cu picks 67 or 68 for 0)
+    //   64: 32 lanes x 2 targets;  65 / 69 / 70: 8 / 4 / 2 lanes x 4 targets
     const bool cont = a.need_cont;
-    if (a.group >= 66 && a.group <= 68) {  // 8 / 4 / 2 lanes x 2 targets (16-, 8-, 4-target groups)
-      const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
-      if (a.group == 66) {
-        if (cont) k_walk2<8, 1, true><<<grid2, 256, 0, s>>>(P);
-        else k_walk2<8, 1, false><<<grid2, 256, 0, s>>>(P);
-      } else if (a.group == 67) {
-        if (cont) k_walk2<4, 1, true><<<grid2, 256, 0, s>>>(P);
-        else k_walk2<4, 1, false><<<grid2, 256, 0, s>>>(P);
-      } else {
-        if (cont) k_walk2<2, 1, true><<<grid2, 256, 0, s>>>(P);
-        else k_walk2<2, 1, false><<<grid2, 256, 0, s>>>(P);
-      }
-    } else if (a.group == 65 || a.group == 69 || a.group == 70) {  // 4 targets per lane
-      const unsigned g4 = (unsigned)((a.n_targets + 1023) / 1024);
-      if (a.group == 65) {
-        if (cont) k_walk2<8, 2, true><<<g4, 256, 0, s>>>(P);
-        else k_walk2<8, 2, false><<<g4, 256, 0, s>>>(P);
-      } else if (a.group == 69) {
-        if (cont) k_walk2<4, 2, true><<<g4, 256, 0, s>>>(P);
-        else k_walk2<4, 2, false><<<g4, 256, 0, s>>>(P);
-      } else {
-        if (cont) k_walk2<2, 2, true><<<g4, 256, 0, s>>>(P);
-        else k_walk2<2, 2, false><<<g4, 256, 0, s>>>(P);
-      }
-    } else {
-      const unsigned grid2 = (unsigned)((a.n_targets + 511) / 512);
-      if (a.group == 64) {
-        if (cont) k_walk2<32, 1, true><<<grid2, 256, 0, s>>>(P);
-        else k_walk2<32, 1, false><<<grid2, 256, 0, s>>>(P);
-      } else {  // default: 4 lanes x 2 targets = 8-target groups (fastest on cfg3-cfg5)
-        if (cont) k_walk2<4, 1, true><<<grid2, 256, 0, s>>>(P);
-        else k_walk2<4, 1, false><<<grid2, 256, 0, s>>>(P);
-      }
+    constexpr int WB = BH_WALK2_BLOCK;
+    const unsigned grid2 = (unsigned)((a.n_targets + 2 * WB - 1) / (2 * WB));
+    const unsigned g4 = (unsigned)((a.n_targets + 4 * WB - 1) / (4 * WB));
+#define BH_WALK2_LAUNCH(GLv, NPv, gr)                          \
+  if (cont) k_walk2<GLv, NPv, true><<<gr, WB, 0, s>>>(P);     \
+  else k_walk2<GLv, NPv, false><<<gr, WB, 0, s>>>(P);
+    switch (a.group) {
+      case 64: BH_WALK2_LAUNCH(32, 1, grid2) break;
+      case 65: BH_WALK2_LAUNCH(8, 2, g4) break;
+      case 66: BH_WALK2_LAUNCH(8, 1, grid2) break;
+      case 68: BH_WALK2_LAUNCH(2, 1, grid2) break;
+      case 69: BH_WALK2_LAUNCH(4, 2, g4) break;
+      case 70: BH_WALK2_LAUNCH(2, 2, g4) break;
+      default: BH_WALK2_LAUNCH(4, 1, grid2) break;  // 67
     }
+#undef BH_WALK2_LAUNCH
   } else {
 #define BH_WALK_CASE(g)                                                     \
   case g:                                                                   \
