@@ -317,6 +317,22 @@ def ours_arm(args):
                "ms_per_step": t_e / e_steps * 1e3,
                "path": "bh_set_state(pinned host) + bh_step(1) + bh_get_state(pinned host) per step"}
 
+    # ownership balance for P = 2/4/8 from this GPU's per-particle costs (the
+    # last walk's interaction counts, storage order): the even Morton-range split
+    # of the multi-GPU path vs the equal-cost split of bh_set_partition
+    balance = None
+    if world == 1:
+        costs, _ = bh.get_own()
+        costs = costs.astype(np.float64)
+        balance = {"cost": "interactions per particle, last walk"}
+        for P in (2, 4, 8):
+            even = [cfg.n * r // P for r in range(P + 1)]
+            cb = bdist.cost_bounds(costs, P)
+            per_e = np.array([costs[even[r]:even[r + 1]].sum() for r in range(P)])
+            per_c = np.array([costs[cb[r]:cb[r + 1]].sum() for r in range(P)])
+            balance[f"P{P}"] = {"even_max_over_mean": float(per_e.max() / per_e.mean()),
+                                "cost_split_max_over_mean": float(per_c.max() / per_c.mean())}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = run_oracle_sample(cfg, m, p, v, args.cpu_samples, 1, 0)
@@ -358,6 +374,7 @@ def ours_arm(args):
             "gpu_launches": int(launches),
             "ms_per_step_graph_replay": ms_graph,
             "clocks": clocks,
+            "ownership_balance": balance,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

@@ -160,6 +160,22 @@ bh_status bh_get_moments(bh_ctx *ctx, double *M, double *MX, int64_t cap);
  * summed over this rank (NULL ok). */
 bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total);
 
+/* Ownership (multi-GPU load balance; the paper's dynamic
+ * load-balancing theme).  Rank r owns the storage ids
+ * [bounds[r], bounds[r+1]) (storage id = the particle's step-0 Morton rank);
+ * bh_create starts from the even split n r / P.
+ * bh_get_own: this rank's own slice in storage order -- icount[own] (the last
+ *   walk's per-particle interactions, a cost estimate; NULL ok) and vel[own][3]
+ *   (the staggered velocities; NULL ok).  where = BH_HOST / BH_DEVICE.  Syncs.
+ * bh_set_partition: new bounds[world + 1] (identical on every rank; 0 = bounds[0]
+ *   <= ... <= bounds[world] = n) and the velocities of the new own slice
+ *   vel[bounds[r+1] - bounds[r]][3] in storage order (gathered by the caller,
+ *   e.g. paper_1109_5190_b200.dist.rebalance).  The own range may hold at most
+ *   2 ceil(n / P) + 1 particles (BH_ERR_ARG otherwise).  Positions are
+ *   replicated and unaffected; results do not depend on the partition.  Syncs. */
+bh_status bh_get_own(bh_ctx *ctx, uint32_t *icount, float *vel, int where);
+bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel, int where);
+
 typedef struct {
     int64_t n_records;      /* walk records: tree nodes + bucket members          */
     int64_t n_internal;     /* internal nodes incl. buckets                       */

@@ -100,6 +100,8 @@ def load_library(path: str = LIB_PATH):
             "bh_get_tree": (i32, [vp, vp, vp, vp, i64, C.POINTER(i64)]),
             "bh_get_moments": (i32, [vp, vp, vp, i64]),
             "bh_get_interactions": (i32, [vp, vp, vp]),
+            "bh_get_own": (i32, [vp, vp, vp, i32]),
+            "bh_set_partition": (i32, [vp, vp, vp, i32]),
             "bh_get_stats": (i32, [vp, C.POINTER(BhStats)]),
             "bh_set_profiling": (i32, [vp, i32]),
             "bh_set_walk_stats": (i32, [vp, i32]),
@@ -283,6 +285,21 @@ class BarnesHut:
         tot = C.c_uint64(0)
         self._chk(self.L.bh_get_interactions(self.h, _ptr(c), C.c_void_p(C.addressof(tot))))
         return c, int(tot.value)
+
+    def get_own(self):
+        """(icount[own], vel[own][3]) of this rank's own slice, storage order."""
+        st = self.get_stats()
+        m = int(st["own_end"] - st["own_begin"])
+        c = np.zeros(m, np.uint32)
+        v = np.zeros((m, 3), np.float32)
+        self._chk(self.L.bh_get_own(self.h, _ptr(c), _ptr(v), BH_HOST))
+        return c, v
+
+    def set_partition(self, bounds, vel_own):
+        """New ownership bounds[world + 1] and the new own slice's velocities."""
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        v = np.ascontiguousarray(vel_own, dtype=np.float32).reshape(-1, 3)
+        self._chk(self.L.bh_set_partition(self.h, _ptr(b), _ptr(v) if v.size else None, BH_HOST))
 
     def get_stats(self) -> dict:
         s = BhStats()

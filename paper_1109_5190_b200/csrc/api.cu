@@ -33,6 +33,7 @@ struct bh_ctx {
   cudaStream_t stream;
   bool own_stream;
   int64_t own_lo, own_hi;
+  std::vector<int64_t> bounds;  // ownership: rank r owns storage ids [bounds[r], bounds[r+1])
   int64_t steps;
   bool tree_valid;
   bool walked;
@@ -91,7 +92,10 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
   L.cap_int = L.cap_rec - n;
   L.cap_resume = n / 8 > 65536 ? n / 8 : 65536;
   if (L.cap_resume > n) L.cap_resume = n;
-  L.n_own_max = (n + world - 1) / world + 1;
+  // velocities of the own slice; room for 2x the even share so that
+  // bh_set_partition can move the boundaries (equal-cost splits)
+  L.n_own_max = 2 * ((n + world - 1) / world) + 1;
+  if (L.n_own_max > n) L.n_own_max = n;
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
   size_t sz[23] = {
@@ -196,6 +200,21 @@ __global__ void k_load_state(float4 *__restrict__ pos4, float4 *__restrict__ vel
 }
 
 // user-order outputs from storage slots [lo, hi): out[uid[s]] = src(s)
+// own-slice velocities [k][3] (storage order) -> vel4[k]
+__global__ void k_vel3to4(float4 *__restrict__ vel4, const float *__restrict__ v3, int64_t m) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) vel4[k] = make_float4(v3[3 * k], v3[3 * k + 1], v3[3 * k + 2], 0.f);
+}
+__global__ void k_vel4to3(float *__restrict__ v3, const float4 *__restrict__ vel4, int64_t m) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) {
+    const float4 v = vel4[k];
+    v3[3 * k] = v.x;
+    v3[3 * k + 1] = v.y;
+    v3[3 * k + 2] = v.z;
+  }
+}
+
 __global__ void k_scatter3(float *__restrict__ out, const float4 *__restrict__ src4, const float *__restrict__ src3,
                            const uint32_t *__restrict__ uid, int64_t lo, int64_t hi, int src_offset_lo) {
   int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -423,8 +442,9 @@ static bh_status exchange(bh_ctx *ctx) {
   const int64_t n = ctx->p.n;
   const int P = ctx->p.world;
   if (ncclGroupStart() != ncclSuccess) return fail(ctx, BH_ERR_NCCL, "ncclGroupStart failed");
+  (void)n;
   for (int r = 0; r < P; r++) {
-    int64_t lo = n * r / P, hi = n * (r + 1) / P;
+    const int64_t lo = ctx->bounds[r], hi = ctx->bounds[r + 1];
     if (hi <= lo) continue;
     float *buf = (float *)(ctx->W.pos4 + lo);
     ncclResult_t rc = ncclBroadcast(buf, buf, (size_t)(hi - lo) * 4, ncclFloat, r, comm, ctx->stream);
@@ -516,6 +536,8 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   const int64_t n = p->n;
   ctx->own_lo = n * p->rank / p->world;
   ctx->own_hi = n * (p->rank + 1) / p->world;
+  ctx->bounds.resize((size_t)p->world + 1);
+  for (int r = 0; r <= p->world; r++) ctx->bounds[r] = n * r / p->world;
   ctx->steps = 0;
   ctx->tree_valid = false;
   ctx->walked = false;
@@ -867,6 +889,55 @@ bh_status bh_get_moments(bh_ctx *ctx, double *M, double *MX, int64_t cap) {
   if (!ctx->tree_valid && ctx->steps == 0) return fail(ctx, BH_ERR_STATE, "no tree built yet");
   int64_t nn = 0;
   return export_tree(ctx, nullptr, nullptr, nullptr, M, MX, cap, &nn);
+}
+
+bh_status bh_get_own(bh_ctx *ctx, uint32_t *icount, float *vel, int where) {
+  if (!ctx || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  const int64_t lo = ctx->own_lo, own_n = ctx->own_hi - ctx->own_lo;
+  cudaStream_t s = ctx->stream;
+  const cudaMemcpyKind kind = where == BH_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (icount && own_n) CK(cudaMemcpyAsync(icount, ctx->W.icount + lo, (size_t)own_n * 4, kind, s));
+  if (vel && own_n) {
+    float *dst = where == BH_DEVICE ? vel : ctx->W.accu;
+    k_vel4to3<<<blocks_for(own_n), 256, 0, s>>>(dst, ctx->W.vel4, own_n);
+    CK(cudaGetLastError());
+    if (where == BH_HOST) CK(cudaMemcpyAsync(vel, ctx->W.accu, (size_t)own_n * 12, cudaMemcpyDeviceToHost, s));
+  }
+  return do_sync(ctx);
+}
+
+bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel, int where) {
+  if (!ctx || !bounds || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  const int P = ctx->p.world, r = ctx->p.rank;
+  const int64_t n = ctx->p.n;
+  if (bounds[0] != 0 || bounds[P] != n) return fail(ctx, BH_ERR_ARG, "bounds must run from 0 to n");
+  for (int k = 0; k < P; k++)
+    if (bounds[k + 1] < bounds[k]) return fail(ctx, BH_ERR_ARG, "bounds must not decrease");
+  const int64_t lo = bounds[r], hi = bounds[r + 1], own_n = hi - lo;
+  if (own_n > ctx->lay.n_own_max)
+    return fail(ctx, BH_ERR_ARG, "own range of %lld exceeds the velocity capacity %lld (2x the even share)",
+                (long long)own_n, (long long)ctx->lay.n_own_max);
+  if (own_n > 0 && !vel) return fail(ctx, BH_ERR_ARG, "velocities of the new own range required");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  cudaStream_t s = ctx->stream;
+  if (own_n > 0) {
+    const float *dv = vel;
+    if (where == BH_HOST) {
+      CK(cudaMemcpyAsync(ctx->W.accu, vel, (size_t)own_n * 12, cudaMemcpyHostToDevice, s));
+      dv = ctx->W.accu;
+    }
+    k_vel3to4<<<blocks_for(own_n), 256, 0, s>>>(ctx->W.vel4, dv, own_n);
+    CK(cudaGetLastError());
+  }
+  for (int k = 0; k <= P; k++) ctx->bounds[k] = bounds[k];
+  ctx->own_lo = lo;
+  ctx->own_hi = hi;
+  drop_graphs(ctx);  // the walk's target range is baked into the captured steps
+  ctx->walked = false;
+  return do_sync(ctx);
 }
 
 bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total) {

@@ -34,6 +34,62 @@ def exchange_plan(n: int, world: int):
     return out
 
 
+def cost_bounds(costs, world: int):
+    """Equal-cost ownership split: bounds[world + 1] over
+    storage order such that every rank's summed cost is as close as possible to
+    total / world.  Rank r ends at the first storage id whose inclusive cost
+    prefix reaches (r + 1) total / world.  Pure function of the costs, so every
+    rank computes the same bounds.  Each range is capped at the velocity
+    capacity 2 ceil(n / world) + 1 of the library."""
+    import numpy as np
+
+    c = np.asarray(costs, dtype=np.float64)
+    n = c.shape[0]
+    cap = min(n, 2 * (-(-n // world)) + 1)
+    pre = np.cumsum(c)
+    total = pre[-1] if n else 0.0
+    b = [0]
+    for r in range(1, world):
+        target = total * r / world
+        e = int(np.searchsorted(pre, target, side="left")) + 1 if total > 0 else n * r // world
+        e = max(b[-1], min(e, n))
+        e = min(e, b[-1] + cap)                      # this rank's capacity
+        e = max(e, n - cap * (world - r))            # the remaining ranks' capacity
+        b.append(e)
+    b.append(n)
+    return b
+
+
+def rebalance(bh, dist, device=None):
+    """Collective: gather every rank's per-particle costs (the last walk's
+    interaction counts) and velocities, compute equal-cost bounds, and hand each
+    rank its new range and velocities (bh_set_partition).  Returns the bounds."""
+    import numpy as np
+    import torch
+
+    world = dist.get_world_size()
+    st = bh.get_stats()
+    lo, hi = int(st["own_begin"]), int(st["own_end"])
+    cnt, vel = bh.get_own()
+    sizes = [None] * world
+    dist.all_gather_object(sizes, (lo, hi))
+    m = max(h - l for l, h in sizes)
+    pad_c = torch.zeros(m, dtype=torch.float64, device=device)
+    pad_v = torch.zeros((m, 3), dtype=torch.float32, device=device)
+    pad_c[: hi - lo] = torch.from_numpy(cnt.astype(np.float64)).to(device)
+    pad_v[: hi - lo] = torch.from_numpy(vel).to(device)
+    all_c = [torch.empty_like(pad_c) for _ in range(world)]
+    all_v = [torch.empty_like(pad_v) for _ in range(world)]
+    dist.all_gather(all_c, pad_c)
+    dist.all_gather(all_v, pad_v)
+    costs = np.concatenate([all_c[r][: h - l].cpu().numpy() for r, (l, h) in enumerate(sizes)])
+    vels = np.concatenate([all_v[r][: h - l].cpu().numpy() for r, (l, h) in enumerate(sizes)])
+    bounds = cost_bounds(costs, world)
+    me = dist.get_rank()
+    bh.set_partition(bounds, vels[bounds[me]:bounds[me + 1]])
+    return bounds
+
+
 def share_nccl_id(make_id, dist) -> bytes:
     """Rank 0 makes the 128-byte ncclUniqueId; every rank receives it."""
     obj = [make_id() if dist.get_rank() == 0 else None]

@@ -79,3 +79,75 @@ def test_partition_edges():
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(hi - lo in (n // world, n // world + 1) for lo, hi in rs)
             assert sum(hi - lo for _, lo, hi in bdist.exchange_plan(n, world)) == n
+
+
+def test_cost_bounds_properties():
+    """Equal-cost ownership split (bh_set_partition's input): covers [0, n),
+    non-decreasing, every range within the library's velocity capacity, and
+    per-rank costs within one particle's cost of total / P."""
+    rng = np.random.default_rng(0)
+    for n, world in [(1000, 2), (30001, 3), (50000, 8), (17, 4)]:
+        costs = rng.integers(100, 3000, size=n).astype(np.float64)
+        costs[: n // 5] *= 4  # a dense region
+        b = bdist.cost_bounds(costs, world)
+        assert b[0] == 0 and b[-1] == n and len(b) == world + 1
+        assert all(b[i] <= b[i + 1] for i in range(world))
+        cap = min(n, 2 * (-(-n // world)) + 1)
+        assert all(b[i + 1] - b[i] <= cap for i in range(world))
+        per = np.array([costs[b[i]:b[i + 1]].sum() for i in range(world)])
+        assert per.max() - costs.sum() / world <= costs.max() + 1e-9 or n < 4 * world
+        assert b == bdist.cost_bounds(costs.copy(), world)  # deterministic
+    # equal costs give the even split
+    assert bdist.cost_bounds(np.ones(12), 3) == [0, 4, 8, 12]
+
+
+class _FakeBH:
+    """Stands in for BarnesHut in the host-side rebalance: an own slice of
+    costs and velocities over a known global array."""
+
+    def __init__(self, n, rank, world, costs, vel):
+        self.lo, self.hi = bdist.own_range(n, rank, world)
+        self.costs, self.vel = costs, vel
+        self.got = None
+
+    def get_stats(self):
+        return {"own_begin": self.lo, "own_end": self.hi}
+
+    def get_own(self):
+        return self.costs[self.lo:self.hi].astype(np.uint32), self.vel[self.lo:self.hi]
+
+    def set_partition(self, bounds, vel_own):
+        self.got = (list(bounds), np.array(vel_own))
+
+
+def _rebalance_worker(rank, world, port, n, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(5)
+        costs = rng.integers(1, 1000, size=n)
+        vel = rng.standard_normal((n, 3)).astype(np.float32)
+        bh = _FakeBH(n, rank, world, costs, vel)
+        bounds = bdist.rebalance(bh, dist)
+        b, v = bh.got
+        ok = (b == list(bounds) == bdist.cost_bounds(costs, world)
+              and np.array_equal(v, vel[b[rank]:b[rank + 1]]))
+        out_q.put((rank, ok, b))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 1001), (3, 5000)])
+def test_gloo_rebalance_host_logic(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rebalance_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res)
+    assert len({tuple(b) for _, _, b in res}) == 1  # every rank holds the same bounds

@@ -384,3 +384,44 @@ def test_near_sorted_path_matches_full_sort(BH, monkeypatch):
     o = _oracle(m, p[perm], v[perm], prm)
     ok, operm = o.keys()
     assert np.array_equal(ka, ok) and np.array_equal(pa.astype(np.int64), operm)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partition_cost_split_bitwise(BH, world):
+    """Equal-cost ownership (bh_set_partition with bounds from the last walk's
+    interaction counts, dist.cost_bounds): every rank's forces, positions and
+    velocities after a step are bitwise the P = 1 ones; the velocities handed
+    over survive the move."""
+    from paper_1109_5190_b200 import dist as bdist
+
+    m, p, v = bhgen.generate("cfg2", n=30000)
+    prm = bhgen.params("cfg2")
+    one = BH(m, p, v, **prm)
+    one.build_tree()
+    ref = one.compute_forces()
+    costs, vel_all = one.get_own()  # P = 1: every particle, storage order
+    _, perm = one.get_keys()        # storage order == step-0 Morton order
+    one.step(1)
+    ref_pos, ref_vel = one.get_state()
+    bounds = bdist.cost_bounds(costs, world)
+    assert bounds != [len(m) * r // world for r in range(world + 1)]  # a real move
+    got = np.full_like(ref, np.nan)
+    got_pos = np.full_like(ref, np.nan)
+    got_vel = np.full_like(ref, np.nan)
+    for r in range(world):
+        bh = BH(m, p, v, rank=r, world=world, **prm)
+        bh.set_partition(bounds, vel_all[bounds[r]:bounds[r + 1]])
+        st = bh.get_stats()
+        assert (st["own_begin"], st["own_end"]) == (bounds[r], bounds[r + 1])
+        assert np.array_equal(bh.get_own()[1], vel_all[bounds[r]:bounds[r + 1]])
+        own = perm[bounds[r]:bounds[r + 1]].astype(np.int64)
+        bh.build_tree()
+        a = bh.compute_forces()
+        got[own] = a[own]
+        bh.step(1)
+        pos, vel = bh.get_state()
+        got_pos[own] = pos[own]
+        got_vel[own] = vel[own]
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref)
+    assert np.array_equal(got_pos, ref_pos) and np.array_equal(got_vel, ref_vel)
