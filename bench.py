@@ -229,6 +229,17 @@ def ours_arm(args):
     # warm-up (untimed)
     bh.step(args.warmup)
     bh.sync()
+    if world > 1 and not args.no_rebalance:
+        # equal-cost ownership from the warm-up's interaction counts (dist.rebalance),
+        # then one more untimed step on the new partition
+        try:
+            bounds = bdist.rebalance(bh, dist, device=f"cuda:{device}")
+            if rank == 0:
+                print(f"rebalanced ownership: {bounds}", file=sys.stderr)
+        except Exception as e:  # keep the even split
+            print(f"rebalance skipped: {e}", file=sys.stderr)
+        bh.step(1)
+        bh.sync()
     st0 = bh.get_stats()
     bh.set_profiling(True)
     barrier()
@@ -397,6 +408,7 @@ def main(argv=None):
     ap.add_argument("--walk-group", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rebalance", action="store_true", help="N > 1: keep the even Morton-range split")
     ap.add_argument("--cpu-samples", type=int, default=20000)
     ap.add_argument("--ref-samples", type=int, default=8192)
     args = ap.parse_args(argv)
