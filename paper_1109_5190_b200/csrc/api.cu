@@ -121,7 +121,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
       (size_t)L.cap_rec * 32,                  // 19 rec_mom
       (size_t)L.cap_int * 4,                   // 20 lvl_list
       (size_t)n * 4,                           // 21 redo list
-      ((size_t)n / 2 + 64) * 4,                // 22 walk group costs (groups of >= 2 targets)
+      (size_t)n * 4,                           // 22 walk cost per particle (its group's trips)
   };
   size_t off = 0;
   for (int i = 0; i < 23; i++) {
@@ -595,7 +595,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
     // storage order is the step-0 Morton order: the previous order of the first
     // build's near-sorted path is the identity (vals[0] always holds a permutation)
     k_iota<<<blocks_for(n), 256, 0, s>>>(ctx->W.vals[0], n);
-    if (cudaMemsetAsync(ctx->W.gcost, 0, ((size_t)n / 2 + 64) * 4, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
+    if (cudaMemsetAsync(ctx->W.gcost, 0, (size_t)n * 4, s) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "memset failed"); break; }
     st = do_sync(ctx);
   } while (0);
   if (st != BH_OK) {

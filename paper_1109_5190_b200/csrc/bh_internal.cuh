@@ -109,7 +109,7 @@ struct Workspace {
   float *accu;        // n * 3, user order (BH_HOST force output staging)
   uint32_t *targets;  // own sorted positions (world > 1)
   uint32_t *redo;     // target slots whose fp32 MAC filter was inconclusive
-  uint32_t *gcost;    // walk cost (union-walk trips) of each target group of k_walk2, last walk
+  uint32_t *gcost;    // per storage id: union-walk trips of its k_walk2 group in the last walk
   uint32_t *scan_tmp; // scan tile partials
   uint32_t *sort_hist;    // 8 x 256
   uint32_t *sort_status;  // 8 passes x tiles x 256

@@ -59,7 +59,7 @@ struct WalkParams {
   float4 *pos4;
   float4 *vel4;
   float *acc_out;  // mode 0: acc_out[3 uid[s]] (user_order) or acc_out[3 (s - own_lo)]
-  uint32_t *gcost;  // k_walk2: last-walk trips per target group (or null)
+  uint32_t *gcost;  // k_walk2: per storage id, the last-walk trips of its group (or null)
   int user_order;
   int64_t n_targets;
   int use_targets;
@@ -376,7 +376,8 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 ? BH_WALK2_MINB : 4) 
   const uint32_t Wn = P.st->n_records;
   const uint32_t chunk = blockIdx.x;
   // Group order.  The block's 256 / GL groups are dealt to its warps in
-  // descending order of their last-walk cost (union-walk iterations, gcost):
+  // descending order of their predicted cost (union-walk trips in the last
+  // walk, kept per particle in gcost):
   // a warp runs until its slowest group is done, so warps of similar groups
   // idle less (the groups themselves -- which targets walk together -- do not
   // change, hence neither do the results).  Without costs: Morton order.
@@ -387,7 +388,21 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 ? BH_WALK2_MINB : 4) 
     __shared__ uint32_t s_cost[GPB], s_perm[GPB];
     const int64_t g0 = (int64_t)chunk * GPB;
     const int64_t ngroups = (P.n_targets + GL * TPL - 1) / (GL * TPL);
-    if (threadIdx.x < GPB) s_cost[threadIdx.x] = g0 + threadIdx.x < ngroups ? P.gcost[g0 + threadIdx.x] : 0u;
+    if (threadIdx.x < GPB) {
+      // a group's predicted cost: the last-walk cost recorded on its first and
+      // last targets (costs travel with the particles, groups are re-formed
+      // from the current Morton order every step)
+      uint32_t cst = 0u;
+      const int64_t g = g0 + threadIdx.x;
+      if (g < ngroups) {
+        const int64_t t0 = g * (GL * TPL);
+        const int64_t t1 = min(t0 + GL * TPL, P.n_targets) - 1;
+        const uint32_t p0 = P.use_targets ? P.targets[t0] : (uint32_t)t0;
+        const uint32_t p1 = P.use_targets ? P.targets[t1] : (uint32_t)t1;
+        cst = max(P.gcost[P.vals[p0]], P.gcost[P.vals[p1]]);
+      }
+      s_cost[threadIdx.x] = cst;
+    }
     __syncthreads();
     if (threadIdx.x < GPB) {
       const uint32_t ci = s_cost[threadIdx.x];
@@ -499,7 +514,11 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 ? BH_WALK2_MINB : 4) 
     git += live ? 1u : 0u;
     if (!__any_sync(full, live)) break;
   }
-  if (P.gcost && gl == 0 && anyv) P.gcost[gidx] = git;
+  if (P.gcost) {
+#pragma unroll
+    for (int k = 0; k < TPL; k++)
+      if (v[k]) P.gcost[T[k].s] = git;  // this walk's cost of the target's group
+  }
   unsigned long long wc = 0;
   bool redo[TPL];
 #pragma unroll
