@@ -95,7 +95,7 @@ def main():
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--command", default="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline")
-    ap.add_argument("--exclude", default="k_walk<32, 1>",
+    ap.add_argument("--exclude", default="k_walk<32, 1>;k_vel4to3;k_relabel;k_pack;k_iota",
                     help="semicolon-separated kernels launched outside the timed steps (shares also shown without them)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
@@ -116,8 +116,8 @@ def main():
             step = "untimed helper" if k in excl else f"{100 * v / Ts:.2f}%"
             md.append(f"| `{k}` | {cnt[k]} | {v:.3f} | {100 * v / T:.2f}% | {step} |")
         md.append("")
-        md.append(f"Excluded from the step shares: {', '.join(excl) or 'nothing'} (launched outside bh_step, e.g. "
-                  "the untimed stats walk bench.py runs once for the flop model).")
+        md.append(f"Excluded from the step shares: {', '.join(excl) or 'nothing'} (launched outside bh_step: the untimed stats walk bench.py runs once for the flop model, "
+                  "bh_create's relabelling, the ownership-balance read-out).")
         md.append("")
         js["launch_share"] = {k: v / T for k, v in tot.items()}
         js["launch_share_step"] = {k: v / Ts for k, v in tot.items() if k not in excl}
