@@ -106,19 +106,30 @@ def test_cfg3_full_step0_and_one_step(BH):
     assert relerr(gpos, opos).max() < TOL
 
 
-@pytest.mark.parametrize("cfg", ["cfg4"])
-def test_full_size_sampled(BH, cfg):
-    """BASELINE full size (N = 2^24) in the bench's launch configuration:
-    keys / permutation / topology bit-exact over all N, forces on 2048 sampled
-    targets, counts integer-exact."""
+@pytest.mark.parametrize("cfg,ntar", [("cfg4", 2048), ("cfg5", 1024)])
+def test_full_size_sampled(BH, cfg, ntar):
+    """BASELINE full sizes (N = 2^24, 2^26) in the bench's launch configuration:
+    keys / permutation / topology bit-exact over all N, forces on sampled
+    targets, counts integer-exact; then (cfg4) one GPU step and the same check
+    teacher-forced on the GPU's new state (reading L24: keys, tree and forces
+    of that state), which exercises the near-sorted sort at full size."""
     m, p, v = bhgen.generate(cfg)
     prm = bhgen.params(cfg)
     bh = BH(m, p, v, **prm)
     bh.build_tree()
     o = _oracle(m, p, v, prm)
     rng = np.random.default_rng(7)
-    targets = np.sort(rng.choice(m.shape[0], 2048, replace=False))
+    targets = np.sort(rng.choice(m.shape[0], ntar, replace=False))
     check_step0(bh, o, m.shape[0], targets=targets)
+    o.close()
+    if cfg != "cfg4":
+        return
+    bh.step(1)
+    pos1, vel1 = bh.get_state()
+    bh.build_tree()
+    assert bh.get_stats()["near_sorted"] == 1
+    o1 = _oracle(m, pos1, vel1, prm)
+    check_step0(bh, o1, m.shape[0], targets=targets)
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 4097, 5000])
