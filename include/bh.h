@@ -174,6 +174,16 @@ bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total);
  *   2 ceil(n / P) + 1 particles (BH_ERR_ARG otherwise).  Positions are
  *   replicated and unaffected; results do not depend on the partition.  Syncs. */
 bh_status bh_get_own(bh_ctx *ctx, uint32_t *icount, float *vel, int where);
+
+/* The replicated positions as the exchange moves them: pos4[k] = (x, y, z, m)
+ * of storage id lo + k, k < hi - lo (storage order, float[hi-lo][4]).  With no
+ * NCCL communicator (nccl_comm = NULL) bh_step skips K8, and a caller can run
+ * its own exchange (MPI, host, or -- in tests/test_gpu_parity.py -- several
+ * single-GPU ranks in one process): after every step, copy each owner's
+ * [bounds[r], bounds[r+1]) slice into every other rank.  bh_set_pos4
+ * invalidates the tree.  Both sync. */
+bh_status bh_get_pos4(bh_ctx *ctx, float *pos4, int64_t lo, int64_t hi, int where);
+bh_status bh_set_pos4(bh_ctx *ctx, const float *pos4, int64_t lo, int64_t hi, int where);
 bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel, int where);
 
 typedef struct {

@@ -101,6 +101,8 @@ def load_library(path: str = LIB_PATH):
             "bh_get_moments": (i32, [vp, vp, vp, i64]),
             "bh_get_interactions": (i32, [vp, vp, vp]),
             "bh_get_own": (i32, [vp, vp, vp, i32]),
+            "bh_get_pos4": (i32, [vp, vp, i64, i64, i32]),
+            "bh_set_pos4": (i32, [vp, vp, i64, i64, i32]),
             "bh_set_partition": (i32, [vp, vp, vp, i32]),
             "bh_get_stats": (i32, [vp, C.POINTER(BhStats)]),
             "bh_set_profiling": (i32, [vp, i32]),
@@ -294,6 +296,16 @@ class BarnesHut:
         v = np.zeros((m, 3), np.float32)
         self._chk(self.L.bh_get_own(self.h, _ptr(c), _ptr(v), BH_HOST))
         return c, v
+
+    def get_pos4(self, lo, hi):
+        """Storage-order slice [lo, hi) of the replicated (x, y, z, m)."""
+        out = np.zeros((max(0, hi - lo), 4), np.float32)
+        self._chk(self.L.bh_get_pos4(self.h, _ptr(out), int(lo), int(hi), BH_HOST))
+        return out
+
+    def set_pos4(self, a, lo, hi):
+        a = np.ascontiguousarray(a, dtype=np.float32).reshape(-1, 4)
+        self._chk(self.L.bh_set_pos4(self.h, _ptr(a), int(lo), int(hi), BH_HOST))
 
     def set_partition(self, bounds, vel_own):
         """New ownership bounds[world + 1] and the new own slice's velocities."""

@@ -940,6 +940,29 @@ bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel,
   return do_sync(ctx);
 }
 
+bh_status bh_get_pos4(bh_ctx *ctx, float *pos4, int64_t lo, int64_t hi, int where) {
+  if (!ctx || !pos4 || lo < 0 || hi > ctx->p.n || hi < lo || (where != BH_HOST && where != BH_DEVICE))
+    return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  if (hi > lo)
+    CK(cudaMemcpyAsync(pos4, ctx->W.pos4 + lo, (size_t)(hi - lo) * 16,
+                       where == BH_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+  return do_sync(ctx);
+}
+
+bh_status bh_set_pos4(bh_ctx *ctx, const float *pos4, int64_t lo, int64_t hi, int where) {
+  if (!ctx || !pos4 || lo < 0 || hi > ctx->p.n || hi < lo || (where != BH_HOST && where != BH_DEVICE))
+    return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  if (hi > lo)
+    CK(cudaMemcpyAsync(ctx->W.pos4 + lo, pos4, (size_t)(hi - lo) * 16,
+                       where == BH_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->tree_valid = false;
+  return do_sync(ctx);
+}
+
 bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total) {
   if (!ctx) return BH_ERR_ARG;
   bh_status st = set_dev(ctx);

@@ -436,3 +436,49 @@ def test_partition_cost_split_bitwise(BH, world):
     assert not np.isnan(got).any()
     assert np.array_equal(got, ref)
     assert np.array_equal(got_pos, ref_pos) and np.array_equal(got_vel, ref_vel)
+
+
+@pytest.mark.parametrize("world,rebalance_at", [(2, None), (3, 2)])
+def test_multirank_steps_external_exchange_bitwise(BH, world, rebalance_at):
+    """The multi-GPU step loop with P single-GPU ranks in one process: each rank
+    builds the full tree, walks and integrates its own range; the exchange of
+    K8 is done by the caller (bh_get_pos4 / bh_set_pos4: every owner's slice to
+    every rank) instead of NCCL.  After 4 steps -- with an equal-cost
+    repartition in between for P = 3 -- every particle's position and velocity
+    is bitwise the P = 1 trajectory."""
+    from paper_1109_5190_b200 import dist as bdist
+
+    m, p, v = bhgen.generate("cfg2", n=20000)
+    prm = bhgen.params("cfg2")
+    n = m.shape[0]
+    one = BH(m, p, v, **prm)
+    one.build_tree()
+    _, perm = one.get_keys()  # step 0: storage id -> user index (storage order = step-0 Morton order)
+    one.step(4)
+    ref_pos, ref_vel = one.get_state()
+    ranks = [BH(m, p, v, rank=r, world=world, **prm) for r in range(world)]
+    bounds = [n * r // world for r in range(world + 1)]
+    for k in range(4):
+        if rebalance_at is not None and k == rebalance_at:
+            costs = np.concatenate([bh.get_own()[0] for bh in ranks]).astype(np.float64)
+            vels = np.concatenate([bh.get_own()[1] for bh in ranks])
+            bounds = bdist.cost_bounds(costs, world)
+            for r, bh in enumerate(ranks):
+                bh.set_partition(bounds, vels[bounds[r]:bounds[r + 1]])
+        for bh in ranks:
+            bh.step(1)
+        slices = [ranks[r].get_pos4(bounds[r], bounds[r + 1]) for r in range(world)]
+        for q, bh in enumerate(ranks):
+            for r in range(world):
+                if r != q:
+                    bh.set_pos4(slices[r], bounds[r], bounds[r + 1])
+    got_pos = np.full_like(ref_pos, np.nan)
+    got_vel = np.full_like(ref_vel, np.nan)
+    for r, bh in enumerate(ranks):
+        pos, vel = bh.get_state()
+        own = perm[bounds[r]:bounds[r + 1]].astype(np.int64)
+        got_pos[own] = pos[own]
+        got_vel[own] = vel[own]
+        # the replicated positions agree everywhere, not only on the own range
+        assert np.array_equal(pos, ref_pos)
+    assert np.array_equal(got_pos, ref_pos) and np.array_equal(got_vel, ref_vel)
