@@ -92,15 +92,18 @@ def test_full_config_parity_free_running(BH, cfg):
     assert st["steps"] == c.steps
 
 
-def test_cfg3_full_step0_and_one_step(BH):
+def test_cfg3_full_step0_and_stated_steps(BH):
+    """cfg3 (2^20, theta = 0.7): step 0 bit-exact + forces over all N, then the
+    BASELINE's 5 steps free-running on both sides: positions <= 1e-4."""
     m, p, v = bhgen.generate("cfg3")
     prm = bhgen.params("cfg3")
     bh = BH(m, p, v, **prm)
     bh.build_tree()
     o = _oracle(m, p, v, prm)
     check_step0(bh, o, m.shape[0])
-    bh.step(2)
-    o.step(2)
+    steps = bhgen.CONFIGS["cfg3"].steps
+    bh.step(steps)
+    o.step(steps)
     gpos, _ = bh.get_state()
     opos, _ = o.state()
     assert relerr(gpos, opos).max() < TOL
@@ -110,9 +113,9 @@ def test_cfg3_full_step0_and_one_step(BH):
 def test_full_size_sampled(BH, cfg, ntar):
     """BASELINE full sizes (N = 2^24, 2^26) in the bench's launch configuration:
     keys / permutation / topology bit-exact over all N, forces on sampled
-    targets, counts integer-exact; then (cfg4) one GPU step and the same check
-    teacher-forced on the GPU's new state (reading L24: keys, tree and forces
-    of that state), which exercises the near-sorted sort at full size."""
+    targets, counts integer-exact; then (cfg4) the stated 5 GPU steps and the
+    same check teacher-forced on the GPU's state (reading L24: keys, tree and
+    forces of that state), which exercises the near-sorted sort at full size."""
     m, p, v = bhgen.generate(cfg)
     prm = bhgen.params(cfg)
     bh = BH(m, p, v, **prm)
@@ -124,7 +127,7 @@ def test_full_size_sampled(BH, cfg, ntar):
     o.close()
     if cfg != "cfg4":
         return
-    bh.step(1)
+    bh.step(bhgen.CONFIGS[cfg].steps)  # the BASELINE's 5 steps
     pos1, vel1 = bh.get_state()
     bh.build_tree()
     assert bh.get_stats()["near_sorted"] == 1
