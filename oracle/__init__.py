@@ -15,6 +15,9 @@ Parity status of every oracle function (DESIGN.md §4 lists the pins):
   leapfrog          -- pinned (constant-acceleration closed form, Kepler orbit,
                        energy drift)
   direct sum        -- pinned (closed forms, Newton's third law)
+  quadrupoles       -- pinned (closed form of two masses, flat sum about the
+                       com, tracelessness; third-order convergence of the
+                       cell field against exact two-body forces)
 """
 from __future__ import annotations
 
@@ -63,6 +66,9 @@ def lib():
         L.oracle_step.argtypes = [vp, i64, vp]
         L.oracle_get_state.argtypes = [vp, vp, vp]
         L.oracle_direct.argtypes = [i64, vp, vp, f64, f64, i64, vp, vp]
+        L.oracle_set_multipole.argtypes = [vp, C.c_int]
+        L.oracle_get_quadrupoles.restype = i64
+        L.oracle_get_quadrupoles.argtypes = [vp, vp, i64]
         L.oracle_interleave.restype = C.c_uint64
         L.oracle_interleave.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
         L.oracle_quantise.restype = C.c_uint32
@@ -84,7 +90,7 @@ class OracleError(RuntimeError):
 class Oracle:
     """fp64 Barnes-Hut state (user order).  Inputs are promoted exactly."""
 
-    def __init__(self, mass, pos, vel=None, *, theta, eps, G=1.0, dt=1e-3, k0=0):
+    def __init__(self, mass, pos, vel=None, *, theta, eps, G=1.0, dt=1e-3, k0=0, multipole=1):
         L = lib()
         self.n = int(np.asarray(mass).shape[0])
         self._m = np.ascontiguousarray(mass, dtype=np.float64)
@@ -94,6 +100,8 @@ class Oracle:
                                   float(theta), float(eps), float(G), float(dt), int(k0))
         if not self._h:
             raise OracleError(OR_ERR_ARG, "oracle_create failed")
+        if multipole != 1:
+            self._chk(L.oracle_set_multipole(self._h, int(multipole)))
         self.built = False
 
     def close(self):
@@ -139,6 +147,15 @@ class Oracle:
         if with_moments:
             return lv, fi, co, M, MX
         return lv, fi, co
+
+    def quadrupoles(self):
+        """Q[node, 6] (xx yy zz xy xz yz) in the tree export order (multipole = 2)."""
+        k = lib().oracle_get_quadrupoles(self._h, None, 0)
+        if k < 0:
+            raise OracleError(OR_ERR_ARG, "no quadrupoles (multipole = 1 or tree not built)")
+        Q = np.zeros((k, 6), np.float64)
+        lib().oracle_get_quadrupoles(self._h, _p(Q), k)
+        return Q
 
     def forces(self, targets=None):
         """(acc[nt,3] fp64 with G applied, interactions[nt]) for user-index targets."""

@@ -25,6 +25,11 @@
  *  7. Leapfrog (kick-drift, deferred closing kick)  (PAPER.md:461-463
  *     "compute the next iteration values"; L8)
  *  8. O(N^2) direct sum                 (SPEC.md:213-221 accel_direct)
+ *  9. Optional quadrupole moments       ("incorporating
+ *     multipole moments" as future work; reading L25 of
+ *     DESIGN.md §3): traceless Q about each cell's centre of mass, combined
+ *     bottom-up in child order by the parallel-axis rule, and the softened
+ *     monopole + quadrupole field of every accepted cell
  *
  * Parity pins: every function here is checked by tests/test_oracle_pins.py
  * against closed forms, brute force on tiny inputs and the worked example
@@ -53,12 +58,14 @@ typedef struct onode {
     int64_t inl;            /* inline storage for the first member           */
     int64_t first, count;   /* sorted range covered (set by DFS numbering)   */
     double M, MX[3], com[3];
+    double Q[6];            /* traceless quadrupole about com: xx yy zz xy xz yz */
 } onode;
 
 typedef struct oracle_ctx {
     int64_t n;
     double *mass, *pos, *vel; /* fp64 state, user order */
     double theta, eps, G, dt;
+    int multipole; /* 1: monopole cells (the paper's method), 2: + quadrupole */
     int64_t k; /* steps taken (0: next kick is the half kick) */
     /* tree state (valid after oracle_build) */
     int built;
@@ -210,6 +217,46 @@ static int64_t number_dfs(onode *nd, int64_t *next_first) {
 /* Moments (L14): leaf M = m, MX = m*x (exact in fp64); internal node and
  * bucket: sequential left-to-right sums over children in digit order (bucket
  * members in sorted order) starting from 0; com = MX / M. */
+/* Step 9.  The traceless quadrupole of a point mass m at offset y from the
+ * expansion centre, m (3 y y^T - |y|^2 I), added to Q in the order xx yy zz xy
+ * xz yz; a cell's Q about its centre of mass is the sum over its children in
+ * digit order of (child Q about the child's com) + (the child's mass at the
+ * offset d = com_child - com) -- the parallel-axis rule, exact because each
+ * child's mass dipole about its own com vanishes.  Particles (single leaves,
+ * bucket members) are point masses with Q = 0 about themselves. */
+static void add_point_quad(double *Q, double m, const double *y) {
+    double r2 = y[0] * y[0];
+    r2 = r2 + y[1] * y[1];
+    r2 = r2 + y[2] * y[2];
+    Q[0] = Q[0] + m * (3.0 * y[0] * y[0] - r2);
+    Q[1] = Q[1] + m * (3.0 * y[1] * y[1] - r2);
+    Q[2] = Q[2] + m * (3.0 * y[2] * y[2] - r2);
+    Q[3] = Q[3] + m * (3.0 * y[0] * y[1]);
+    Q[4] = Q[4] + m * (3.0 * y[0] * y[2]);
+    Q[5] = Q[5] + m * (3.0 * y[1] * y[2]);
+}
+
+static void quadrupole(oracle_ctx *c, onode *nd) {
+    for (int k = 0; k < 6; k++) nd->Q[k] = 0.0;
+    if (nd->is_leaf) {
+        for (int64_t t = 0; t < nd->nmemb; t++) {
+            int64_t u = c->perm[nd->memb[t]];
+            double y[3];
+            for (int a = 0; a < 3; a++) y[a] = c->pos[3 * u + a] - nd->com[a];
+            add_point_quad(nd->Q, c->mass[u], y);
+        }
+        return;
+    }
+    for (int d = 0; d < 8; d++) {
+        onode *ch = nd->child[d];
+        if (!ch) continue;
+        for (int k = 0; k < 6; k++) nd->Q[k] = nd->Q[k] + ch->Q[k];
+        double y[3];
+        for (int a = 0; a < 3; a++) y[a] = ch->com[a] - nd->com[a];
+        add_point_quad(nd->Q, ch->M, y);
+    }
+}
+
 static void moments(oracle_ctx *c, onode *nd) {
     nd->M = 0.0;
     nd->MX[0] = nd->MX[1] = nd->MX[2] = 0.0;
@@ -230,6 +277,7 @@ static void moments(oracle_ctx *c, onode *nd) {
         }
     }
     for (int a = 0; a < 3; a++) nd->com[a] = nd->MX[a] / nd->M;
+    if (c->multipole >= 2) quadrupole(c, nd);
 }
 
 /* ---------------------------------------------------------------- steps 5-6 */
@@ -260,6 +308,28 @@ static void contribute(const oracle_ctx *c, walker *w, double m, const double *s
     w->count++;
 }
 
+/* An accepted cell with multipole = 2: the monopole contribution, then the
+ * quadrupole field of the softened potential -(G/2) r^T Q r / r_e^5 (r = x -
+ * com, r_e^2 = |r|^2 + eps^2), written with dr = com - x:
+ *   a_q = -(Q dr) / r_e^5 + (5/2) (dr^T Q dr) dr / r_e^7        (G applied last) */
+static void contribute_cell(const oracle_ctx *c, walker *w, const onode *nd) {
+    contribute(c, w, nd->M, nd->com);
+    if (c->multipole < 2) return;
+    double dr[3];
+    for (int a = 0; a < 3; a++) dr[a] = nd->com[a] - w->x[a];
+    double r2 = dist2(nd->com, w->x) + c->eps * c->eps;
+    if (r2 == 0.0) { w->nonfinite = 1; return; }
+    const double *Q = nd->Q;
+    double q[3];
+    q[0] = Q[0] * dr[0] + Q[3] * dr[1] + Q[4] * dr[2];
+    q[1] = Q[3] * dr[0] + Q[1] * dr[1] + Q[5] * dr[2];
+    q[2] = Q[4] * dr[0] + Q[5] * dr[1] + Q[2] * dr[2];
+    double s = q[0] * dr[0] + q[1] * dr[1] + q[2] * dr[2];
+    double inv2 = 1.0 / r2, inv = sqrt(inv2);
+    double inv5 = inv2 * inv2 * inv, inv7 = inv5 * inv2;
+    for (int a = 0; a < 3; a++) w->acc[a] = w->acc[a] - q[a] * inv5 + 2.5 * s * inv7 * dr[a];
+}
+
 static void contribute_particle(const oracle_ctx *c, walker *w, int64_t sp) {
     int64_t u = c->perm[sp];
     contribute(c, w, c->mass[u], &c->pos[3 * u]);
@@ -285,7 +355,7 @@ static void walk(const oracle_ctx *c, const onode *nd, walker *w) {
     int contains = nd->first <= w->ki && w->ki < nd->first + nd->count;
     /* L5: a cell containing the target is never accepted */
     if (!contains && mac_accept(c, nd, w->x)) {
-        contribute(c, w, nd->M, nd->com);
+        contribute_cell(c, w, nd);
         return;
     }
     if (nd->is_leaf) { /* bucket: its children are its member particles */
@@ -324,7 +394,35 @@ oracle_ctx *oracle_create(int64_t n, const double *mass, const double *pos, cons
     memcpy(c->pos, pos, (size_t)n * 3 * sizeof(double));
     if (vel) memcpy(c->vel, vel, (size_t)n * 3 * sizeof(double));
     c->theta = theta; c->eps = eps; c->G = G; c->dt = dt; c->k = k0;
+    c->multipole = 1;
     return c;
+}
+
+/* Multipole order of accepted cells (1 = the paper's monopole, default;
+ * 2 = + quadrupole).  Takes effect at the next oracle_build. */
+int oracle_set_multipole(oracle_ctx *c, int order) {
+    if (!c || order < 1 || order > 2) return OR_ERR_ARG;
+    c->multipole = order;
+    c->built = 0;
+    return OR_OK;
+}
+
+/* Quadrupoles of the exported nodes (DFS order as oracle_get_tree), Q[6] each
+ * (xx yy zz xy xz yz); returns the node count. */
+static void export_quad(const onode *nd, double *Q, int64_t *at) {
+    for (int k = 0; k < 6; k++) Q[6 * *at + k] = nd->Q[k];
+    (*at)++;
+    if (nd->is_leaf) return;
+    for (int d = 0; d < 8; d++)
+        if (nd->child[d]) export_quad(nd->child[d], Q, at);
+}
+
+int64_t oracle_get_quadrupoles(const oracle_ctx *c, double *Q, int64_t cap) {
+    if (!c->built || c->multipole < 2) return -1;
+    if (!Q || cap < c->n_nodes) return c->n_nodes;
+    int64_t at = 0;
+    export_quad(c->root, Q, &at);
+    return at;
 }
 
 void oracle_destroy(oracle_ctx *c) {

@@ -392,3 +392,92 @@ def test_energy_drift_theta0():
     e1 = _energy(m64, x, vh + a * dt / 2, eps)
     assert abs(e1 - e0) / abs(e0) < 1e-3
     assert abs(e0) > 0.1  # a bound system (Plummer: E ~ -0.19 in these units)
+
+
+# ---------------------------------------------------------------- quadrupoles
+# (multipole = 2: SURVEY.md §8(f) NEXT-3, "incorporating
+# multipole moments"; reading L25 of DESIGN.md §3)
+
+def test_quadrupole_two_masses_closed_form():
+    """m1 = 1 at x = 0, m2 = 3 at x = 1: com 0.75, offsets -0.75 and 0.25;
+    Q = sum m (3 y y - |y|^2 I) = diag(1.5, -0.75, -0.75) exactly."""
+    m = np.array([1.0, 3.0])
+    p = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    o = oracle.Oracle(m, p, theta=0.5, eps=0.0, multipole=2).build()
+    Q = o.quadrupoles()
+    assert np.array_equal(Q[0], [1.5, -0.75, -0.75, 0.0, 0.0, 0.0])
+    lv, fi, co = o.tree()
+    assert np.all(Q[co == 1] == 0.0)  # particles: no quadrupole about themselves
+
+
+def test_quadrupole_parallel_axis_equals_flat_sum():
+    """Every node's Q (combined bottom-up in child order) equals the flat sum
+    over its particles about its centre of mass; traceless; leaves zero."""
+    rng = np.random.default_rng(11)
+    n = 3000
+    m = rng.uniform(0.5, 2.0, n)
+    p = rng.standard_normal((n, 3)) * [1.0, 0.5, 2.0]
+    o = oracle.Oracle(m, p, theta=0.5, eps=0.01, multipole=2).build()
+    lv, fi, co, M, MX = o.tree(with_moments=True)
+    Q = o.quadrupoles()
+    _, perm = o.keys()
+    ps = p.astype(np.float64)[perm]  # sorted order (the oracle's fp64 state of fp32? no: fp64 input)
+    ms = m[perm]
+    for k in rng.choice(len(lv), 400, replace=False):
+        sl = slice(fi[k], fi[k] + co[k])
+        com = MX[k] / M[k]
+        y = ps[sl] - com
+        r2 = (y * y).sum(1)
+        flat = np.array([(ms[sl] * (3 * y[:, 0] * y[:, 0] - r2)).sum(), (ms[sl] * (3 * y[:, 1] * y[:, 1] - r2)).sum(),
+                         (ms[sl] * (3 * y[:, 2] * y[:, 2] - r2)).sum(), (ms[sl] * 3 * y[:, 0] * y[:, 1]).sum(),
+                         (ms[sl] * 3 * y[:, 0] * y[:, 2]).sum(), (ms[sl] * 3 * y[:, 1] * y[:, 2]).sum()])
+        scale = (ms[sl] * r2).sum() + 1e-300
+        assert np.abs(Q[k] - flat).max() <= 1e-12 * scale + 1e-300
+        assert abs(Q[k][0] + Q[k][1] + Q[k][2]) <= 1e-12 * scale + 1e-300
+
+
+def _cluster_and_target(dist, seed=3):
+    rng = np.random.default_rng(seed)
+    a = 1.0
+    cl = rng.uniform(0.0, a, (6, 3))
+    mc = rng.uniform(0.5, 2.0, 6)
+    tgt = np.array([[1.0, 1.0, 1.0]]) / np.sqrt(3.0) * dist + 0.5 * a
+    return np.concatenate([mc, [1.0]]), np.concatenate([cl, tgt])
+
+
+@pytest.mark.parametrize("order,expect", [(1, 4.0), (2, 8.0)])
+def test_cell_field_convergence_order(order, expect):
+    """A compact cluster seen as one cell from a far target: the relative error
+    of the target's acceleration against the exact (direct) sum falls like
+    (a/d)^2 for the monopole and (a/d)^3 with the quadrupole -- a wrong sign or
+    factor in the quadrupole field breaks the cubic rate."""
+    errs = []
+    for d in (16.0, 32.0, 64.0):
+        m, p = _cluster_and_target(d)
+        o = oracle.Oracle(m, p, theta=0.9, eps=0.0, multipole=order).build()
+        acc, cnt = o.forces(np.array([6]))
+        assert cnt[0] == 1  # the cluster is one accepted cell
+        ref = oracle.direct(m, p, 0.0, targets=np.array([6]))
+        errs.append(np.linalg.norm(acc[0] - ref[0]) / np.linalg.norm(ref[0]))
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert 0.75 * expect < r1 < 1.3 * expect and 0.75 * expect < r2 < 1.3 * expect, (errs, r1, r2)
+    if order == 2:
+        m, p = _cluster_and_target(16.0)
+        mono = oracle.Oracle(m, p, theta=0.9, eps=0.0).build().forces(np.array([6]))[0][0]
+        quad = oracle.Oracle(m, p, theta=0.9, eps=0.0, multipole=2).build().forces(np.array([6]))[0][0]
+        ref = oracle.direct(m, p, 0.0, targets=np.array([6]))[0]
+        assert np.linalg.norm(quad - ref) < 0.2 * np.linalg.norm(mono - ref)
+
+
+def test_quadrupole_theta0_is_direct_and_counts_unchanged():
+    """theta = 0 accepts no cell: quadrupole mode is the direct sum; at any
+    theta the interaction counts (the MAC decisions) do not depend on the order."""
+    m, p, v = bhgen.generate("cfg1")
+    pd = p.astype(np.float64)
+    o2 = oracle.Oracle(m, pd, theta=0.0, eps=1e-3, multipole=2).build()
+    a2, _ = o2.forces(np.arange(0, 4096, 97))
+    ref = oracle.direct(m, pd, 1e-3, targets=np.arange(0, 4096, 97))
+    assert np.abs(a2 - ref).max() <= 1e-12 * np.abs(ref).max()
+    c1 = oracle.Oracle(m, pd, theta=0.5, eps=1e-3).build().forces()[1]
+    c2 = oracle.Oracle(m, pd, theta=0.5, eps=1e-3, multipole=2).build().forces()[1]
+    assert np.array_equal(c1, c2)
