@@ -40,6 +40,7 @@ METRIC = "BH interactions/s and particles/s per step at 1/2/4/8 B200; % FP32 pea
 UNIT = "interactions/s"
 FLOP_PER_INTERACTION = 18  # dx,dy,dz 3 + d2 5 + r2 1 + rsqrt^3 2 + M* 1 + acc 6 (rsqrt itself not counted)
 FLOP_PER_OPEN = 8          # the MAC distance of a node that is opened: 3 sub + 5
+FLOP_PER_QUAD = 38         # multipole = 2: Q dr 15, dr.Q dr 5, inv^5 / inv^7 4, 2.5 s inv^7 2, accumulate 12
 
 
 def env_rank():
@@ -212,7 +213,7 @@ def ours_arm(args):
     m, p, v = bhgen.generate(cfg)
     prm = bhgen.params(cfg)
     bh = BarnesHut(m, p, v, device=device, rank=rank, world=world, nccl_comm=comm, walk_group=args.walk_group,
-                   **prm)
+                   multipole=args.multipole, **prm)
     stream = bh.stream
     props = torch.cuda.get_device_properties(device)
     sms = props.multi_processor_count
@@ -285,7 +286,8 @@ def ours_arm(args):
 
     # roofline of the dominant kernel (the walk), measured live with CUDA events
     walk_ms = prof["ms"]["walk"] / args.steps
-    flops_walk_launch = (FLOP_PER_INTERACTION * inter_local + FLOP_PER_OPEN * opens_local) / args.steps
+    fpi = FLOP_PER_INTERACTION + (FLOP_PER_QUAD if args.multipole == 2 else 0)
+    flops_walk_launch = (fpi * inter_local + FLOP_PER_OPEN * opens_local) / args.steps
     achieved_tf = flops_walk_launch / (walk_ms / 1e3) / 1e12
     peaks = measured_peaks()
     sm_max = peaks.get("sm_max_mhz", 1965.0)
@@ -358,6 +360,7 @@ def ours_arm(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(workload_config(cfg, m, p, v), parallelism=f"morton-range x{world}",
+                           multipole=args.multipole,
                            walk_group=args.walk_group,
                            walk_kernel=(("k_walk2<4,1>: 8-target groups, 4 lanes x 2 targets"
                                          if cfg.theta < 0.6 and cfg.n >= (1 << 22)
@@ -373,8 +376,10 @@ def ours_arm(args):
                          "peak_source": f"derived: 2 flop x 128 FP32 lanes x {sms} SMs x {sm_max:.0f} MHz "
                                         "(sm_max_mhz of MEASURED_PEAKS.json; B200_PROFILING.md)",
                          "flops_per_launch": flops_walk_launch, "launch_ms": walk_ms,
-                         "flop_model": "18 per interaction + 8 per opened node (opens/interaction ratio from an "
-                                       "untimed stats walk on the final state)"},
+                         "flop_model": (f"{fpi} per interaction" + (" (18 monopole + 38 quadrupole, evaluated for "
+                                                                     "every interaction)" if args.multipole == 2 else "")
+                                        + " + 8 per opened node (opens/interaction ratio from an untimed stats walk "
+                                          "on the final state)")},
             "hbm_stages": {"keys_sort_GBps": sort_gbs,
                            "keys_sort_bytes_model": ("near-sorted path: 88 B/particle + the out-of-order keys' passes"
                                                      if near else "K1 32 B + 8 passes x 24 B per particle"),
@@ -406,6 +411,8 @@ def main(argv=None):
     ap.add_argument("--config", default="cfg4", choices=sorted(bhgen.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--walk-group", type=int, default=0)
+    ap.add_argument("--multipole", type=int, default=1, choices=[1, 2],
+                    help="2: cells carry quadrupoles (SURVEY.md §8(f) NEXT-3); 1: the paper's monopole (default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true", help="N > 1: keep the even Morton-range split")

@@ -85,6 +85,11 @@ typedef struct {
                            80..85 = persistent lane groups (80: 1 x 4, 81: 1 x 2, 82: 2 x 4,
                            83: 2 x 2, 84: 4 x 2, 85: 4 x 4 lanes x targets), 90..95 = the same
                            groups without persistence (one group per slot)                 */
+    int multipole;      /* cell expansion: 0 or 1 = monopole (the paper's method); 2 = monopole
+                           + traceless quadrupole about the cell's centre of mass (the paper's
+                           future work; reading L25 of DESIGN.md §3).  The MAC
+                           and the interaction counts do not change; with 2, walk_group must be
+                           0, 1-32 or 64-70                                                    */
 } bh_params;
 
 /* Bytes of device workspace the ctx needs for these params (n, world,
@@ -174,6 +179,11 @@ bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total);
  *   2 ceil(n / P) + 1 particles (BH_ERR_ARG otherwise).  Positions are
  *   replicated and unaffected; results do not depend on the partition.  Syncs. */
 bh_status bh_get_own(bh_ctx *ctx, uint32_t *icount, float *vel, int where);
+
+/* multipole = 2: the fp64 quadrupoles of the tree nodes in bh_get_tree's order,
+ * Q[node][6] = (xx, yy, zz, xy, xz, yz) about the node's centre of mass
+ * (particles: 0).  Q may be NULL to query *n_nodes.  Syncs. */
+bh_status bh_get_quadrupoles(bh_ctx *ctx, double *Q, int64_t cap, int64_t *n_nodes);
 
 /* The replicated positions as the exchange moves them: pos4[k] = (x, y, z, m)
  * of storage id lo + k, k < hi - lo (storage order, float[hi-lo][4]).  With no

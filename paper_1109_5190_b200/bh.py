@@ -41,6 +41,7 @@ class BhParams(C.Structure):
         ("workspace_bytes", C.c_size_t),
         ("node_capacity", C.c_int64),
         ("walk_group", C.c_int),
+        ("multipole", C.c_int),
     ]
 
 
@@ -101,6 +102,7 @@ def load_library(path: str = LIB_PATH):
             "bh_get_moments": (i32, [vp, vp, vp, i64]),
             "bh_get_interactions": (i32, [vp, vp, vp]),
             "bh_get_own": (i32, [vp, vp, vp, i32]),
+            "bh_get_quadrupoles": (i32, [vp, vp, i64, C.POINTER(i64)]),
             "bh_get_pos4": (i32, [vp, vp, i64, i64, i32]),
             "bh_set_pos4": (i32, [vp, vp, i64, i64, i32]),
             "bh_set_partition": (i32, [vp, vp, vp, i32]),
@@ -140,7 +142,7 @@ class BarnesHut:
     """One bh_ctx: a Barnes-Hut simulation state on one device (one rank)."""
 
     def __init__(self, mass, pos, vel=None, *, theta, eps, G=1.0, dt=1e-3, device=0, rank=0, world=1,
-                 nccl_comm=None, node_capacity=0, walk_group=0, stream=None):
+                 nccl_comm=None, node_capacity=0, walk_group=0, stream=None, multipole=1):
         import torch
 
         if not torch.cuda.is_available():
@@ -158,7 +160,7 @@ class BarnesHut:
         p = BhParams(n=n, theta=float(theta), eps=float(eps), G=float(G), dt=float(dt), device=device, rank=rank,
                      world=world, stream=C.c_void_p(self.stream.cuda_stream), nccl_comm=nccl_comm,
                      workspace=None, workspace_bytes=0, node_capacity=int(node_capacity),
-                     walk_group=int(walk_group))
+                     walk_group=int(walk_group), multipole=int(multipole))
         nbytes = self.L.bh_workspace_bytes(C.byref(p))
         if nbytes == 0:
             raise BhError(BH_ERR_ARG, "invalid parameters")
@@ -281,6 +283,14 @@ class BarnesHut:
         MX = np.zeros((m, 3), np.float64)
         self._chk(self.L.bh_get_moments(self.h, _ptr(M), _ptr(MX), m))
         return M, MX
+
+    def get_quadrupoles(self):
+        """fp64 Q[node, 6] (xx yy zz xy xz yz) in get_tree order (multipole = 2)."""
+        nn = C.c_int64(0)
+        self._chk(self.L.bh_get_quadrupoles(self.h, None, 0, C.byref(nn)))
+        Q = np.zeros((nn.value, 6), np.float64)
+        self._chk(self.L.bh_get_quadrupoles(self.h, _ptr(Q), nn.value, C.byref(nn)))
+        return Q
 
     def get_interactions(self):
         c = np.zeros(self.n, np.uint32)

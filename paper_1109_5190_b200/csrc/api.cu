@@ -79,7 +79,7 @@ namespace bh {
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-Layout make_layout(int64_t n, int world, int64_t node_capacity) {
+Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
   Layout L;
   memset(&L, 0, sizeof L);
   L.n = n;
@@ -98,7 +98,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
   if (L.n_own_max > n) L.n_own_max = n;
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-  size_t sz[23] = {
+  size_t sz[25] = {
       sizeof(DevStatus),                       // 0 status
       (size_t)n * 16,                          // 1 pos4
       (size_t)L.n_own_max * 16,                // 2 vel4
@@ -122,9 +122,11 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity) {
       (size_t)L.cap_int * 4,                   // 20 lvl_list
       (size_t)n * 4,                           // 21 redo list
       (size_t)n * 4,                           // 22 walk cost per particle (its group's trips)
+      multipole == 2 ? (size_t)L.cap_rec * 48 : 0,  // 23 quadrupoles fp64 (multipole = 2)
+      multipole == 2 ? (size_t)L.cap_rec * 32 : 0,  // 24 quadrupoles fp32 for the walk
   };
   size_t off = 0;
-  for (int i = 0; i < 23; i++) {
+  for (int i = 0; i < 25; i++) {
     L.off[i] = off;
     off += align_up(sz[i]);
   }
@@ -160,6 +162,8 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.lvl_list = (uint32_t *)(b + L.off[20]);
   W.redo = (uint32_t *)(b + L.off[21]);
   W.gcost = (uint32_t *)(b + L.off[22]);
+  W.qmom = L.off[23] != L.off[24] ? (double *)(b + L.off[23]) : nullptr;
+  W.qrec = L.off[24] != L.total ? (float4 *)(b + L.off[24]) : nullptr;
 }
 
 // ---------------------------------------------------------------- small kernels
@@ -279,6 +283,14 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     snprintf(err, errn, "node_capacity must be 0 or in [n + 1, 2^31 - 2]");
     return BH_ERR_ARG;
   }
+  if (p->multipole < 0 || p->multipole > 2) {
+    snprintf(err, errn, "multipole must be 0, 1 or 2");
+    return BH_ERR_ARG;
+  }
+  if (p->multipole == 2 && p->walk_group >= 80) {
+    snprintf(err, errn, "multipole = 2 needs walk_group 0, 1-32 or 64-70");
+    return BH_ERR_ARG;
+  }
   int g = p->walk_group;
   if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || (g >= 64 && g <= 70) ||
         (g >= 80 && g <= 85) || (g >= 90 && g <= 95))) {
@@ -377,7 +389,7 @@ static bh_status build_tree(bh_ctx *ctx) {
   prof_end(ctx, &pp, (ctx->near_sort ? 22 : 0) + 2 + SORT_PASSES + 1);
   ctx->sort_buf = buf;
   prof_begin(ctx, &pp, 2);
-  CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, s));
+  CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, s));  // (zeroes the particles' quadrupoles)
   prof_end(ctx, &pp, 6);
   prof_begin(ctx, &pp, 3);
   int launches = 0;
@@ -415,6 +427,7 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.kick = kick;
   a.dt = (float)ctx->p.dt;
   a.theta2 = ctx->p.theta * ctx->p.theta;
+  a.quad = ctx->p.multipole == 2;
   a.own_lo = (uint32_t)ctx->own_lo;
   a.acc_out = mode == 0 ? acc_out : nullptr;
   a.user_order = user_order ? 1 : 0;
@@ -484,7 +497,7 @@ extern "C" {
 size_t bh_workspace_bytes(const bh_params *p) {
   char e[128];
   if (validate(p, e, sizeof e) != BH_OK) return 0;
-  return make_layout(p->n, p->world, p->node_capacity).total;
+  return make_layout(p->n, p->world, p->node_capacity, p->multipole).total;
 }
 
 const char *bh_status_string(int st) {
@@ -512,7 +525,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
     snprintf(g_err, sizeof g_err, "need mass, pos and where in {BH_HOST, BH_DEVICE}");
     return BH_ERR_ARG;
   }
-  Layout lay = make_layout(p->n, p->world, p->node_capacity);
+  Layout lay = make_layout(p->n, p->world, p->node_capacity, p->multipole);
   if (!p->workspace || p->workspace_bytes < lay.total || ((uintptr_t)p->workspace & 255)) {
     snprintf(g_err, sizeof g_err, "workspace must be 256-aligned and >= %zu bytes", lay.total);
     return BH_ERR_OOM;
@@ -889,6 +902,32 @@ bh_status bh_get_moments(bh_ctx *ctx, double *M, double *MX, int64_t cap) {
   if (!ctx->tree_valid && ctx->steps == 0) return fail(ctx, BH_ERR_STATE, "no tree built yet");
   int64_t nn = 0;
   return export_tree(ctx, nullptr, nullptr, nullptr, M, MX, cap, &nn);
+}
+
+bh_status bh_get_quadrupoles(bh_ctx *ctx, double *Q, int64_t cap, int64_t *n_nodes) {
+  if (!ctx) return BH_ERR_ARG;
+  if (ctx->p.multipole != 2) return fail(ctx, BH_ERR_STATE, "quadrupoles need multipole = 2");
+  if (!ctx->tree_valid && ctx->steps == 0) return fail(ctx, BH_ERR_STATE, "no tree built yet");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  if (st) return st;
+  const uint32_t nrec = ctx->hstatus->n_records;
+  std::vector<Rec> rec(nrec);
+  std::vector<double> q((size_t)nrec * 6);
+  CK(cudaMemcpy(rec.data(), ctx->W.rec, (size_t)nrec * sizeof(Rec), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(q.data(), ctx->W.qmom, (size_t)nrec * 48, cudaMemcpyDeviceToHost));
+  int64_t k = 0;
+  for (uint32_t c = 0; c < nrec; c++) {
+    const uint4 a = rec[c].aux;
+    if (a.w & META_MEMBER) continue;
+    if (Q && k < cap)
+      for (int j = 0; j < 6; j++) Q[6 * k + j] = (a.w & META_LEAF) ? 0.0 : q[6 * (size_t)c + j];
+    k++;
+  }
+  if (n_nodes) *n_nodes = k;
+  if (Q && k > cap) return fail(ctx, BH_ERR_ARG, "cap %lld < %lld tree nodes", (long long)cap, (long long)k);
+  return BH_OK;
 }
 
 bh_status bh_get_own(bh_ctx *ctx, uint32_t *icount, float *vel, int where) {

@@ -110,6 +110,8 @@ struct Workspace {
   uint32_t *targets;  // own sorted positions (world > 1)
   uint32_t *redo;     // target slots whose fp32 MAC filter was inconclusive
   uint32_t *gcost;    // per storage id: union-walk trips of its k_walk2 group in the last walk
+  double *qmom;       // multipole = 2: per record, fp64 quadrupole xx yy zz xy xz yz (null otherwise)
+  float4 *qrec;       // multipole = 2: per record, 2 float4 = fp32 (xx yy zz xy) (xz yz 0 0)
   uint32_t *scan_tmp; // scan tile partials
   uint32_t *sort_hist;    // 8 x 256
   uint32_t *sort_status;  // 8 passes x tiles x 256
@@ -144,7 +146,7 @@ constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
 
 constexpr int BBOX_BLOCKS = 592;  // 4 x 148 SMs
 
-Layout make_layout(int64_t n, int world, int64_t node_capacity);
+Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole);
 void bind_workspace(const Layout &L, void *base, Workspace &W);
 
 // ---- kernel launchers (each returns cudaGetLastError()) -------------------
@@ -176,6 +178,7 @@ struct WalkArgs {
   float eps2, G;
   float kick, dt;       // mode 1
   double theta2;
+  int quad;             // multipole = 2: add each accepted cell's quadrupole field
   uint32_t own_lo;
   float *acc_out;       // mode 0: [n][3] device output (may be null)
   int user_order;       // 1: acc_out[uid[s]], 0: acc_out[s - own_lo]

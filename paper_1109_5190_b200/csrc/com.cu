@@ -39,10 +39,26 @@ __device__ __forceinline__ float round_down_f(double x) {
   return f;
 }
 
+// multipole = 2 (reading L25; the oracle's step 9): m (3 y y^T - |y|^2 I) of a
+// point mass at offset y, added to Q (xx yy zz xy xz yz) with the oracle's
+// fp64 operation order, so the quadrupoles are bit-identical too
+__device__ __forceinline__ void add_point_quad(double Q[6], double m, double y0, double y1, double y2) {
+  double r2 = __dmul_rn(y0, y0);
+  r2 = __dadd_rn(r2, __dmul_rn(y1, y1));
+  r2 = __dadd_rn(r2, __dmul_rn(y2, y2));
+  Q[0] = __dadd_rn(Q[0], __dmul_rn(m, __dsub_rn(__dmul_rn(__dmul_rn(3.0, y0), y0), r2)));
+  Q[1] = __dadd_rn(Q[1], __dmul_rn(m, __dsub_rn(__dmul_rn(__dmul_rn(3.0, y1), y1), r2)));
+  Q[2] = __dadd_rn(Q[2], __dmul_rn(m, __dsub_rn(__dmul_rn(__dmul_rn(3.0, y2), y2), r2)));
+  Q[3] = __dadd_rn(Q[3], __dmul_rn(m, __dmul_rn(__dmul_rn(3.0, y0), y1)));
+  Q[4] = __dadd_rn(Q[4], __dmul_rn(m, __dmul_rn(__dmul_rn(3.0, y0), y2)));
+  Q[5] = __dadd_rn(Q[5], __dmul_rn(m, __dmul_rn(__dmul_rn(3.0, y1), y2)));
+}
+
 __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatus *__restrict__ st,
                                                        const uint32_t *__restrict__ lvl_list,
                                                        Rec *__restrict__ rec,
-                                                       double4 *__restrict__ rec_mom, double theta) {
+                                                       double4 *__restrict__ rec_mom, double theta,
+                                                       double *__restrict__ qmom, float4 *__restrict__ qrec) {
   if (st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t cnt = st->lvl_count[level];
   const uint32_t off = st->lvl_offset[level];
@@ -76,6 +92,36 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
     const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
     const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
     rec[c].cm = make_float4(fx, fy, fz, __double2float_rn(M));
+    if (qmom) {
+      // the quadrupole about (cx, cy, cz): the children in digit order, each its
+      // own Q plus its mass at its com's offset (parallel-axis rule)
+      double Q[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      uint32_t q = c + 1;
+      while (q < end) {
+        const uint4 ca = rec[q].aux;
+        if (ca.w & META_LEAF) {
+          const float4 pp = rec[q].cm;
+          add_point_quad(Q, (double)pp.w, __dsub_rn((double)pp.x, cx), __dsub_rn((double)pp.y, cy),
+                         __dsub_rn((double)pp.z, cz));
+          q = q + 1;
+        } else {
+          const double *qc = qmom + 6 * (size_t)q;
+#pragma unroll
+          for (int k = 0; k < 6; k++) Q[k] = __dadd_rn(Q[k], qc[k]);
+          const double4 mc = rec_mom[q];
+          add_point_quad(Q, mc.x, __dsub_rn(__ddiv_rn(mc.y, mc.x), cx), __dsub_rn(__ddiv_rn(mc.z, mc.x), cy),
+                         __dsub_rn(__ddiv_rn(mc.w, mc.x), cz));
+          q = ca.z;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 6; k++) qmom[6 * (size_t)c + k] = Q[k];
+      // the walk's copy is -Q in fp32 (walk.cu quad_pair: the minus sign of the
+      // field's first term rides on Q, exactly)
+      qrec[2 * (size_t)c] = make_float4(-__double2float_rn(Q[0]), -__double2float_rn(Q[1]),
+                                        -__double2float_rn(Q[2]), -__double2float_rn(Q[3]));
+      qrec[2 * (size_t)c + 1] = make_float4(-__double2float_rn(Q[4]), -__double2float_rn(Q[5]), 0.f, 0.f);
+    }
     float tacc, trej;
     if (!(theta > 0.0)) {
       tacc = INFINITY;
@@ -115,7 +161,7 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, int64_t cap_rec, int64
   int grid = (int)(need < lim ? need : lim);
   if (grid < 1) grid = 1;
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
-    k_moments_level<<<grid, 256, 0, s>>>(l, W.status, W.lvl_list, W.rec, W.rec_mom, theta);
+    k_moments_level<<<grid, 256, 0, s>>>(l, W.status, W.lvl_list, W.rec, W.rec_mom, theta, W.qmom, W.qrec);
     if (launches) (*launches)++;
   }
   return cudaGetLastError();

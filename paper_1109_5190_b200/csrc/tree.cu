@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
                                               const uint32_t *__restrict__ nstart, const float4 *__restrict__ pos4,
                                               int64_t n, DevStatus *st, Rec *__restrict__ rec,
                                               uint32_t *__restrict__ rec_first,
-                                              uint32_t *__restrict__ lvl_list) {
+                                              uint32_t *__restrict__ lvl_list, float4 *__restrict__ qrec) {
   __shared__ uint32_t cnt[24], slot[24], gb[24];
   if (st->err & ERR_NODE_OVERFLOW) return;  // uniform: nothing safe to write
   if (threadIdx.x < 24) { cnt[threadIdx.x] = 0; slot[threadIdx.x] = 0; }
@@ -138,6 +138,10 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
   rec[c].cm = pos4[vals[p]];
   // T_acc = -inf: a particle record is always "accepted" unless it is the target
   rec[c].aux = make_uint4(__float_as_uint(-INFINITY), __float_as_uint(-INFINITY), c + 1u, meta);
+  if (qrec) {  // multipole = 2: a particle has no quadrupole about itself
+    qrec[2 * (size_t)c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    qrec[2 * (size_t)c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, cudaStream_t s) {
@@ -150,7 +154,7 @@ cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf,
   // cap_int: the level list holds at most cap_rec - n internal nodes
   k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, cap_rec - n, W.status, W.rec);
   k_emit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.lcp, W.nstart, W.pos4, n,
-                                                     W.status, W.rec, W.rec_first, W.lvl_list);
+                                                     W.status, W.rec, W.rec_first, W.lvl_list, W.qrec);
   return cudaGetLastError();
 }
 

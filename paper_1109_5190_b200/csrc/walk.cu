@@ -44,6 +44,8 @@ namespace bh {
 
 struct WalkParams {
   const Rec *__restrict__ rec;
+  const float4 *__restrict__ qrec;  // multipole = 2: -Q (fp32) per record, 2 float4 (else null)
+  int quad;
   const double4 *__restrict__ rec_mom;
   const uint32_t *__restrict__ nstart;
   const uint32_t *__restrict__ vals;
@@ -74,6 +76,36 @@ __device__ __forceinline__ float rsqrt_fast(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// multipole = 2 (reading L25): the quadrupole field of an accepted cell,
+//   a += -(Q dr) / r_e^5 + (5/2) (dr^T Q dr) dr / r_e^7,   dr = (dx, dy, dz),
+// with nq = -Q (the records hold -Q): q = nq dr, s = dr^T q = -(dr^T Q dr),
+// g1 = inv^5, g2 = (-2.5 s) inv^7:  a += g1 q + g2 dr.  Every walk kernel uses
+// this operation sequence (k_walk2 in packed pairs), so they agree bitwise.
+struct QuadRec {
+  float xx, yy, zz, xy, xz, yz;
+};
+__device__ __forceinline__ QuadRec load_quad(const float4 *__restrict__ qrec, uint32_t c) {
+  const float4 a = qrec[2 * (size_t)c], b = qrec[2 * (size_t)c + 1];
+  QuadRec q;
+  q.xx = a.x; q.yy = a.y; q.zz = a.z; q.xy = a.w; q.xz = b.x; q.yz = b.y;
+  return q;
+}
+__device__ __forceinline__ void quad_term(const QuadRec &Q, float dx, float dy, float dz, float inv, bool acc,
+                                          float &ax, float &ay, float &az) {
+  const float qx = __fmaf_rn(Q.xz, dz, __fmaf_rn(Q.xy, dy, __fmul_rn(Q.xx, dx)));
+  const float qy = __fmaf_rn(Q.yz, dz, __fmaf_rn(Q.yy, dy, __fmul_rn(Q.xy, dx)));
+  const float qz = __fmaf_rn(Q.zz, dz, __fmaf_rn(Q.yz, dy, __fmul_rn(Q.xz, dx)));
+  const float sq = __fmaf_rn(qz, dz, __fmaf_rn(qy, dy, __fmul_rn(qx, dx)));
+  const float inv2 = __fmul_rn(inv, inv);
+  const float inv5 = __fmul_rn(__fmul_rn(inv2, inv2), inv);
+  const float inv7 = __fmul_rn(inv5, inv2);
+  const float g1 = acc ? inv5 : 0.0f;  // branch-free, like the monopole's f
+  const float g2 = acc ? __fmul_rn(__fmul_rn(-2.5f, sq), inv7) : 0.0f;
+  ax = __fmaf_rn(g2, dx, __fmaf_rn(g1, qx, ax));
+  ay = __fmaf_rn(g2, dy, __fmaf_rn(g1, qy, ay));
+  az = __fmaf_rn(g2, dz, __fmaf_rn(g1, qz, az));
 }
 
 __device__ __noinline__ bool exact_accept(const double4 *__restrict__ rec_mom, uint32_t c, uint32_t level, float x,
@@ -215,6 +247,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkParams P) {
       ax = fmaf(f, dx, ax);
       ay = fmaf(f, dy, ay);
       az = fmaf(f, dz, az);
+      if (P.quad) quad_term(load_quad(P.qrec, cc), dx, dy, dz, inv, acc, ax, ay, az);
       asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(cnt) : "r"((uint32_t)acc));
       resume = acc ? skip : (amb ? (BH_DROP | cc) : resume);
       uint32_t nxt;
@@ -355,6 +388,41 @@ __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, floa
       : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip), "r"(drop));
 }
 
+// mac_pair that also zeroes the quadrupole factors (g1, g2) of targets that do
+// not accept the record
+__device__ __forceinline__ void mac_pair_q(uint32_t cc, float d2A, float d2B, float tacc, float trej, uint32_t skip,
+                                           uint32_t &resA, uint32_t &resB, uint32_t &cntA, uint32_t &cntB,
+                                           uint32_t &opn, float &fA, float &fB, float &g1A, float &g1B, float &g2A,
+                                           float &g2B) {
+  const uint32_t drop = BH_DROP | cc;
+  asm("{\n\t.reg .pred pa, pc, pq, pb, pd, pr, po;\n\t"
+      "setp.ge.u32 pa, %13, %0;\n\t"
+      "setp.gt.and.f32 pc, %14, %16, pa;\n\t"
+      "setp.ge.and.f32 pq, %14, %17, pa;\n\t"
+      "setp.ge.u32 pb, %13, %1;\n\t"
+      "setp.gt.and.f32 pd, %15, %16, pb;\n\t"
+      "setp.ge.and.f32 pr, %15, %17, pb;\n\t"
+      "@pc add.u32 %2, %2, 1;\n\t"
+      "@pd add.u32 %3, %3, 1;\n\t"
+      "@pq selp.b32 %0, %18, %19, pc;\n\t"
+      "@pr selp.b32 %1, %18, %19, pd;\n\t"
+      "@!pc mov.b32 %5, 0f00000000;\n\t"
+      "@!pd mov.b32 %6, 0f00000000;\n\t"
+      "@!pc mov.b32 %7, 0f00000000;\n\t"
+      "@!pd mov.b32 %8, 0f00000000;\n\t"
+      "@!pc mov.b32 %9, 0f00000000;\n\t"
+      "@!pd mov.b32 %10, 0f00000000;\n\t"
+      "not.pred pq, pq;\n\t"
+      "not.pred pr, pr;\n\t"
+      "and.pred pa, pa, pq;\n\t"
+      "and.pred pb, pb, pr;\n\t"
+      "or.pred po, pa, pb;\n\t"
+      "@po mov.b32 %4, 1;\n\t}"
+      : "+r"(resA), "+r"(resB), "+r"(cntA), "+r"(cntB), "+r"(opn), "+f"(fA), "+f"(fB), "+f"(g1A), "+f"(g1B),
+        "+f"(g2A), "+f"(g2B)
+      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip), "r"(drop));
+}
+
 #ifndef BH_WALK2_BLOCK
 #define BH_WALK2_BLOCK 128
 #endif
@@ -366,8 +434,8 @@ __device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, floa
 #endif
 // NP pairs of targets per lane (2 NP targets), GL lanes per group: a group of
 // 2 NP GL Morton-consecutive targets shares one traversal.
-template <int GL, int NP, bool CONT>
-__global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 ? BH_WALK2_MINB : 4) * 256 / BH_WALK2_BLOCK) k_walk2(const WalkParams P) {
+template <int GL, int NP, bool CONT, bool QUAD>
+__global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 && !QUAD ? BH_WALK2_MINB : 4) * 256 / BH_WALK2_BLOCK) k_walk2(const WalkParams P) {
   constexpr int TPL = 2 * NP;  // targets per lane
   const uint32_t full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -481,18 +549,38 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 ? BH_WALK2_MINB : 4) 
       up2(add2(D2, E2), r2A, r2B);
       const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
       float fA, fB;
-      up2(mul2(mul2(pk2(cm.w, cm.w), mul2(INV, INV)), INV), fA, fB);
+      const F2 INV2 = mul2(INV, INV);
+      up2(mul2(mul2(pk2(cm.w, cm.w), INV2), INV), fA, fB);
+      // multipole = 2: the record's -Q (broadcast) and the quadrupole factors
+      // (quad_term's operation sequence, in pairs)
+      F2 QX, QY, QZ;
+      float g1A = 0.f, g1B = 0.f, g2A = 0.f, g2B = 0.f;
+      if (QUAD) {
+        const float4 qa = __ldg(&P.qrec[2 * (size_t)cc]), qb = __ldg(&P.qrec[2 * (size_t)cc + 1]);
+        // qa = (xx, yy, zz, xy), qb = (xz, yz, -, -)
+        QX = fma2(pk2(qb.x, qb.x), DZ, fma2(pk2(qa.w, qa.w), DY, mul2(pk2(qa.x, qa.x), DX)));
+        QY = fma2(pk2(qb.y, qb.y), DZ, fma2(pk2(qa.y, qa.y), DY, mul2(pk2(qa.w, qa.w), DX)));
+        QZ = fma2(pk2(qa.z, qa.z), DZ, fma2(pk2(qb.y, qb.y), DY, mul2(pk2(qb.x, qb.x), DX)));
+        const F2 SQ = fma2(QZ, DZ, fma2(QY, DY, mul2(QX, DX)));
+        const F2 INV5 = mul2(mul2(INV2, INV2), INV);
+        const F2 INV7 = mul2(INV5, INV2);
+        up2(INV5, g1A, g1B);
+        up2(mul2(mul2(pk2(-2.5f, -2.5f), SQ), INV7), g2A, g2B);
+      }
       // per-target MAC (identical decisions to k_walk); an inconclusive fp32
       // test drops the target out (resume = BH_DROP | c): k_walk_resume continues it
+      // (a record containing the target is opened, never accepted: NaN distance)
+      float qA = d2A, qB = d2B;
       if (CONT) {
-        // a record containing the target is opened, never accepted (NaN
-        // distance: every comparison is false)
         const bool cA = (cc <= Li[a]) & (skip > Li[a]), cB = (cc <= Li[b]) & (skip > Li[b]);
         const float qnan = __int_as_float(0x7fffffff);
-        mac_pair(cc, cA ? qnan : d2A, cB ? qnan : d2B, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA,
-                 fB);
+        qA = cA ? qnan : d2A;
+        qB = cB ? qnan : d2B;
+      }
+      if (QUAD) {
+        mac_pair_q(cc, qA, qB, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA, fB, g1A, g1B, g2A, g2B);
       } else {
-        mac_pair(cc, d2A, d2B, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA, fB);
+        mac_pair(cc, qA, qB, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA, fB);
       }
       const F2 FF = pk2(fA, fB);
       // packed accumulate on (a, b) register pairs (this form avoids ptxas moves)
@@ -502,6 +590,16 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 ? BH_WALK2_MINB : 4) 
           : "+f"(ay[a]), "+f"(ay[b]) : "l"(FF.v), "l"(DY.v));
       asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
           : "+f"(az[a]), "+f"(az[b]) : "l"(FF.v), "l"(DZ.v));
+      if (QUAD) {
+        const F2 G1 = pk2(g1A, g1B), G2 = pk2(g2A, g2B);
+        F2 AX = pk2(ax[a], ax[b]), AY = pk2(ay[a], ay[b]), AZ = pk2(az[a], az[b]);
+        AX = fma2(G2, DX, fma2(G1, QX, AX));
+        AY = fma2(G2, DY, fma2(G1, QY, AY));
+        AZ = fma2(G2, DZ, fma2(G1, QZ, AZ));
+        up2(AX, ax[a], ax[b]);
+        up2(AY, ay[a], ay[b]);
+        up2(AZ, az[a], az[b]);
+      }
     }
     if (GL == 32) {
       c = min(__any_sync(full, opn != 0u) ? cc + 1u : skip, Wn);
@@ -786,6 +884,13 @@ __device__ __forceinline__ bool resume_visit(const WalkParams &P, const Target &
     A.ax += (double)__fmul_rn(f, dx);
     A.ay += (double)__fmul_rn(f, dy);
     A.az += (double)__fmul_rn(f, dz);
+    if (P.quad) {
+      float qx = 0.f, qy = 0.f, qz = 0.f;
+      quad_term(load_quad(P.qrec, c), dx, dy, dz, inv, true, qx, qy, qz);
+      A.ax += (double)qx;
+      A.ay += (double)qy;
+      A.az += (double)qz;
+    }
     A.cnt++;
   } else {
     A.nop++;
@@ -891,6 +996,8 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   if (a.n_targets <= 0) return cudaSuccess;
   WalkParams P;
   P.rec = W.rec;
+  P.quad = a.quad && W.qrec;
+  P.qrec = P.quad ? W.qrec : nullptr;
   P.rec_mom = W.rec_mom;
   P.nstart = W.nstart;
   P.vals = W.vals[a.buf];
@@ -982,9 +1089,14 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
     constexpr int WB = BH_WALK2_BLOCK;
     const unsigned grid2 = (unsigned)((a.n_targets + 2 * WB - 1) / (2 * WB));
     const unsigned g4 = (unsigned)((a.n_targets + 4 * WB - 1) / (4 * WB));
-#define BH_WALK2_LAUNCH(GLv, NPv, gr)                          \
-  if (cont) k_walk2<GLv, NPv, true><<<gr, WB, 0, s>>>(P);     \
-  else k_walk2<GLv, NPv, false><<<gr, WB, 0, s>>>(P);
+#define BH_WALK2_LAUNCH(GLv, NPv, gr)                                              \
+  if (P.quad) {                                                                   \
+    if (cont) k_walk2<GLv, NPv, true, true><<<gr, WB, 0, s>>>(P);                \
+    else k_walk2<GLv, NPv, false, true><<<gr, WB, 0, s>>>(P);                    \
+  } else {                                                                        \
+    if (cont) k_walk2<GLv, NPv, true, false><<<gr, WB, 0, s>>>(P);               \
+    else k_walk2<GLv, NPv, false, false><<<gr, WB, 0, s>>>(P);                   \
+  }
     switch (a.group) {
       case 64: BH_WALK2_LAUNCH(32, 1, grid2) break;
       case 65: BH_WALK2_LAUNCH(8, 2, g4) break;

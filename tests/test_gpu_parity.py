@@ -485,3 +485,51 @@ def test_multirank_steps_external_exchange_bitwise(BH, world, rebalance_at):
         # the replicated positions agree everywhere, not only on the own range
         assert np.array_equal(pos, ref_pos)
     assert np.array_equal(got_pos, ref_pos) and np.array_equal(got_vel, ref_vel)
+
+
+@pytest.mark.parametrize("cfg,n", [("cfg2", 30000), ("cfg3", 40000)])
+def test_quadrupole_parity(BH, cfg, n):
+    """multipole = 2 (NEXT-3, reading L25): keys / tree / fp64 moments AND fp64
+    quadrupoles bit-identical to the extended oracle, interaction counts equal
+    (the MAC does not change), accelerations within 1e-4, two free-running
+    steps within 1e-4 -- and closer to the direct sum than the monopole."""
+    m, p, v = bhgen.generate(cfg, n=n)
+    prm = bhgen.params(cfg)
+    bh = BH(m, p, v, multipole=2, **prm)
+    bh.build_tree()
+    o = oracle.Oracle(m, np.asarray(p, np.float64), np.asarray(v, np.float64), multipole=2, **prm).build()
+    acc, err = check_step0(bh, o, n)
+    assert np.array_equal(bh.get_quadrupoles(), o.quadrupoles()), "fp64 quadrupoles not bit-identical"
+    # more accurate than the monopole against the exact direct sum
+    tg = np.arange(0, n, 97)
+    ref = oracle.direct(m, np.asarray(p, np.float64), prm["eps"], prm["G"], targets=tg)
+    mono = BH(m, p, v, **prm)
+    mono.build_tree()
+    am = mono.compute_forces()
+    e_q = np.median(relerr(acc[tg], ref))
+    e_m = np.median(relerr(am[tg], ref))
+    assert e_q < 0.5 * e_m, (e_q, e_m)
+    # every walk variant that supports it gives bitwise the same forces
+    for g in (1, 32, 64, 66, 67, 68, 70):
+        b = BH(m, p, v, multipole=2, walk_group=g, **prm)
+        b.build_tree()
+        assert np.array_equal(b.compute_forces(), acc), g
+    bh.step(2)
+    o.step(2)
+    assert relerr(bh.get_state()[0], o.state()[0]).max() < TOL
+
+
+def test_quadrupole_arg_checks(BH):
+    from paper_1109_5190_b200.bh import BhError
+
+    m, p, v = bhgen.generate("cfg1")
+    with pytest.raises(BhError) as e:
+        BH(m, p, v, theta=0.5, eps=1e-3, multipole=3)
+    assert e.value.code == -1
+    with pytest.raises(BhError) as e:
+        BH(m, p, v, theta=0.5, eps=1e-3, multipole=2, walk_group=80)
+    assert e.value.code == -1
+    b = BH(m, p, v, theta=0.5, eps=1e-3)
+    b.build_tree()
+    with pytest.raises(BhError):
+        b.get_quadrupoles()  # monopole ctx
