@@ -165,13 +165,20 @@ class BarnesHut:
         if nbytes == 0:
             raise BhError(BH_ERR_ARG, "invalid parameters")
         self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{device}")
+        if os.environ.get("BH_POISON_WORKSPACE"):
+            # test hook: every byte 0xFF (NaN as fp32 / fp64, huge as an index),
+            # so a kernel reading memory nothing wrote this step shows up
+            self.workspace.fill_(0xFF)
         base = self.workspace.data_ptr()
         p.workspace = (base + 255) & ~255
         p.workspace_bytes = nbytes
         self.params = p
         h = C.c_void_p()
+        # the workspace comes from torch's caching allocator, ordered on the
+        # caller's current stream (a reused block may still be in use there, and
+        # the poison fill runs there): the ctx stream starts after it
+        self.stream.wait_stream(torch.cuda.current_stream(device))
         if on_dev:
-            self.stream.wait_stream(torch.cuda.current_stream(device))  # inputs made on the caller's stream
             m_, p_, v_ = (mass.contiguous().float(), pos.contiguous().float(),
                           None if vel is None else vel.contiguous().float())
             rc = self.L.bh_create(C.byref(h), C.byref(p), _ptr(m_), _ptr(p_), _ptr(v_), BH_DEVICE)

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) k_lcp_count(const unsigned long long *__r
 
 // tiny: level offsets, capacity check
 __global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, int64_t cap_rec, int64_t cap_int,
-                              DevStatus *st, Rec *__restrict__ rec) {
+                              DevStatus *st, Rec *__restrict__ rec, float4 *__restrict__ qrec) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint32_t run = 0;
   for (int l = 0; l < 24; l++) {
@@ -74,6 +74,10 @@ __global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, in
   }
   rec[nrec].cm = make_float4(0.f, 0.f, 0.f, 0.f);
   rec[nrec].aux = make_uint4(__float_as_uint(INFINITY), __float_as_uint(INFINITY), nrec, 0u);
+  if (qrec) {  // parked groups visit the sentinel: its quadrupole must be finite (zero)
+    qrec[2 * (size_t)nrec] = make_float4(0.f, 0.f, 0.f, 0.f);
+    qrec[2 * (size_t)nrec + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 // last index q >= start with (keys[q] >> sh) == prefix, given keys[start] matches
@@ -152,7 +156,7 @@ cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf,
   e = launch_scan_u32(W.nstart, n + 1, W.scan_tmp, s);
   if (e != cudaSuccess) return e;
   // cap_int: the level list holds at most cap_rec - n internal nodes
-  k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, cap_rec - n, W.status, W.rec);
+  k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, cap_rec - n, W.status, W.rec, W.qrec);
   k_emit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.lcp, W.nstart, W.pos4, n,
                                                      W.status, W.rec, W.rec_first, W.lvl_list, W.qrec);
   return cudaGetLastError();

@@ -533,3 +533,25 @@ def test_quadrupole_arg_checks(BH):
     b.build_tree()
     with pytest.raises(BhError):
         b.get_quadrupoles()  # monopole ctx
+
+
+@pytest.mark.parametrize("multipole", [1, 2])
+def test_poisoned_workspace_same_results(BH, monkeypatch, multipole):
+    """Every workspace byte set to 0xFF at create (NaN as floats, huge as
+    indices): a kernel that read memory nothing had written would change the
+    results or fault.  Three steps, forces and quadrupoles must be bitwise
+    those of a normal workspace."""
+    m, p, v = bhgen.generate("cfg2", n=25000)
+    prm = bhgen.params("cfg2")
+    ref = BH(m, p, v, multipole=multipole, **prm)
+    monkeypatch.setenv("BH_POISON_WORKSPACE", "1")
+    got = BH(m, p, v, multipole=multipole, **prm)
+    monkeypatch.delenv("BH_POISON_WORKSPACE")
+    for bh in (ref, got):
+        bh.step(3)
+        bh.build_tree()
+    assert np.array_equal(ref.compute_forces(), got.compute_forces())
+    assert np.array_equal(ref.get_state()[0], got.get_state()[0])
+    assert np.array_equal(ref.get_state()[1], got.get_state()[1])
+    if multipole == 2:
+        assert np.array_equal(ref.get_quadrupoles(), got.get_quadrupoles())
