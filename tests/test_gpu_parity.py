@@ -302,9 +302,12 @@ def test_device_pointer_paths(BH):
     assert np.array_equal(po.cpu().numpy(), hp)
 
 
-def test_sort_vs_lexsort_many_ties(BH):
+@pytest.mark.parametrize("near", ["0", "1"])
+def test_sort_vs_lexsort_many_ties(BH, monkeypatch, near):
     """K2 + tie fix-up == numpy lexsort (library routine) on heavy ties, over
-    several steps (ties recur in storage order != user order)."""
+    several steps (ties recur in storage order != user order), on the full
+    radix path and on the near-sorted path."""
+    monkeypatch.setenv("BH_NEAR_SORT" if near == "1" else "BH_NO_NEAR_SORT", "1")
     rng = np.random.default_rng(9)
     pos = rng.integers(0, 16, size=(50000, 3)).astype(np.float32)
     vel = rng.normal(size=(50000, 3)).astype(np.float32)
@@ -370,7 +373,9 @@ def test_near_sorted_path_matches_full_sort(BH, monkeypatch):
     order is lost (positions permuted by set_state)."""
     m, p, v = bhgen.generate("cfg2", n=50000)
     prm = bhgen.params("cfg2")
+    monkeypatch.setenv("BH_NEAR_SORT", "1")  # on below its automatic size threshold too
     a = BH(m, p, v, **prm)
+    monkeypatch.delenv("BH_NEAR_SORT")
     monkeypatch.setenv("BH_NO_NEAR_SORT", "1")
     b = BH(m, p, v, **prm)
     monkeypatch.delenv("BH_NO_NEAR_SORT")
@@ -543,6 +548,7 @@ def test_poisoned_workspace_same_results(BH, monkeypatch, multipole):
     those of a normal workspace."""
     m, p, v = bhgen.generate("cfg2", n=25000)
     prm = bhgen.params("cfg2")
+    monkeypatch.setenv("BH_NEAR_SORT", "1")  # cover the near-sorted path too
     ref = BH(m, p, v, multipole=multipole, **prm)
     monkeypatch.setenv("BH_POISON_WORKSPACE", "1")
     got = BH(m, p, v, multipole=multipole, **prm)
