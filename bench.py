@@ -293,7 +293,8 @@ def ours_arm(args):
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     peak = fp32_peak_tflops(sms, sm_max)
     clocks = clk.summary()
-    traffic, traffic_src = load_traffic("walk", f"{cfg.name}")
+    # the committed ncu capture is of the default (monopole) walk of this config
+    traffic, traffic_src = load_traffic("walk", f"{cfg.name}") if args.multipole == 1 else (None, None)
     phase_ms = {k: vv / args.steps for k, vv in prof["ms"].items()}
     # keys + sort phase: the near-sorted path (previous order) moves 88 B per key
     # (K1' 32, mark 8, split 24, merge 24) + the out-of-order keys' radix passes;
