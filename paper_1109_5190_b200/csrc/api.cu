@@ -292,7 +292,7 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     return BH_ERR_ARG;
   }
   int g = p->walk_group;
-  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || (g >= 64 && g <= 71) ||
+  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || (g >= 64 && g <= 70) ||
         (g >= 80 && g <= 85) || (g >= 90 && g <= 95))) {
     snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16, 32, 64..70, 80..85 or 90..95");
     return BH_ERR_ARG;

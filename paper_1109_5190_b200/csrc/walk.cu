@@ -261,10 +261,6 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.theta2 = a.theta2;
   P.own_lo = a.own_lo;
   P.num_sms = a.num_sms > 0 ? a.num_sms : 148;
-  if (a.group == 71) {  // experiment: group-list statistics only (no forces)
-    const char *gt = getenv("BH_GLIST_GT");
-    return launch_walk_list_stats(P, gt ? atoi(gt) : 64, a.need_cont, a.n_targets, s);
-  }
   if (!a.stats && a.group >= 80 && a.group <= 95) {
     const cudaError_t e = launch_walk_lane(P, a.group, a.need_cont, a.n_targets, s);
     if (e != cudaSuccess) return e;

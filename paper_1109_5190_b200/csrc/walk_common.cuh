@@ -308,6 +308,5 @@ constexpr int RESUME_STACK = BH_RESUME_STACK_N;
 void launch_walk_simple(const WalkParams &P, int group, bool stats, int64_t n_targets, cudaStream_t s);
 cudaError_t launch_walk_lane(const WalkParams &P, int group, bool cont, int64_t n_targets, cudaStream_t s);
 void launch_walk_resume(const WalkParams &P, int64_t n_targets, cudaStream_t s);
-cudaError_t launch_walk_list_stats(const WalkParams &P, int gt, bool cont, int64_t n_targets, cudaStream_t s);
 
 }  // namespace bh
