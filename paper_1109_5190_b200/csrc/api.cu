@@ -98,7 +98,8 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
   if (L.n_own_max > n) L.n_own_max = n;
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-  size_t sz[25] = {
+  L.blocks = (n + 1 + 255) / 256;  // tree.cu's particle blocks
+  size_t sz[30] = {
       sizeof(DevStatus),                       // 0 status
       (size_t)n * 16,                          // 1 pos4
       (size_t)L.n_own_max * 16,                // 2 vel4
@@ -117,16 +118,21 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
       sizeof(float) * 8 * BBOX_BLOCKS,         // 15 bbox partials
       (size_t)L.cap_rec * 32,                  // 16 rec (cm + aux)
       (size_t)L.cap_resume * sizeof(ResumeState),  // 17 walk resume states
-      (size_t)L.cap_rec * 4,                   // 18 rec_first
+      0,                                       // 18 (unused)
       (size_t)L.cap_rec * 32,                  // 19 rec_mom
-      (size_t)L.cap_int * 4,                   // 20 lvl_list
+      (size_t)L.cap_rec * 4,                   // 20 item_rec (level-ordered items)
       (size_t)n * 4,                           // 21 redo list
       (size_t)n * 4,                           // 22 walk cost per particle (its group's trips)
       multipole == 2 ? (size_t)L.cap_rec * 48 : 0,  // 23 quadrupoles fp64 (multipole = 2)
       multipole == 2 ? (size_t)L.cap_rec * 32 : 0,  // 24 quadrupoles fp32 for the walk
+      (size_t)L.cap_rec * 4,                   // 25 item_clo
+      (size_t)L.cap_rec * 4,                   // 26 lvl_skip
+      (size_t)L.cap_rec * 32,                  // 27 lvl_mom
+      multipole == 2 ? (size_t)L.cap_rec * 48 : 0,  // 28 lvl_q
+      (size_t)BH_NLEVELS * (L.blocks + (L.blocks + 1023) / 1024) * 4,  // 29 blkcnt + segment sums (tree.cu)
   };
   size_t off = 0;
-  for (int i = 0; i < 25; i++) {
+  for (int i = 0; i < 30; i++) {
     L.off[i] = off;
     off += align_up(sz[i]);
   }
@@ -157,13 +163,17 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.rec = (Rec *)(b + L.off[16]);
   W.resume = (ResumeState *)(b + L.off[17]);
   W.cap_resume = L.cap_resume;
-  W.rec_first = (uint32_t *)(b + L.off[18]);
   W.rec_mom = (double4 *)(b + L.off[19]);
-  W.lvl_list = (uint32_t *)(b + L.off[20]);
+  W.item_rec = (uint32_t *)(b + L.off[20]);
+  W.item_clo = (uint32_t *)(b + L.off[25]);
+  W.lvl_skip = (uint32_t *)(b + L.off[26]);
+  W.lvl_mom = (double4 *)(b + L.off[27]);
+  W.lvl_q = L.off[28] != L.off[29] ? (double *)(b + L.off[28]) : nullptr;
+  W.blkcnt = (uint32_t *)(b + L.off[29]);
   W.redo = (uint32_t *)(b + L.off[21]);
   W.gcost = (uint32_t *)(b + L.off[22]);
   W.qmom = L.off[23] != L.off[24] ? (double *)(b + L.off[23]) : nullptr;
-  W.qrec = L.off[24] != L.total ? (float4 *)(b + L.off[24]) : nullptr;
+  W.qrec = L.off[24] != L.off[25] ? (float4 *)(b + L.off[24]) : nullptr;
 }
 
 // ---------------------------------------------------------------- small kernels
@@ -390,10 +400,10 @@ static bh_status build_tree(bh_ctx *ctx) {
   ctx->sort_buf = buf;
   prof_begin(ctx, &pp, 2);
   CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, s));  // (zeroes the particles' quadrupoles)
-  prof_end(ctx, &pp, 6);
+  prof_end(ctx, &pp, 8);
   prof_begin(ctx, &pp, 3);
   int launches = 0;
-  CK(launch_moments(ctx->W, n, ctx->lay.cap_rec, ctx->lay.cap_int, ctx->p.theta, s, &launches));
+  CK(launch_moments(ctx->W, n, ctx->p.theta, s, &launches));
   prof_end(ctx, &pp, launches);
   ctx->tree_valid = true;
   return BH_OK;
@@ -859,7 +869,12 @@ static bh_status export_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint3
   std::vector<uint32_t> fst(nrec);
   std::vector<double4> mom;
   CK(cudaMemcpy(rec.data(), ctx->W.rec, (size_t)nrec * sizeof(Rec), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(fst.data(), ctx->W.rec_first, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
+  {  // first particle of each record: particle p owns records [nstart[p], nstart[p+1])
+    std::vector<uint32_t> ns((size_t)n + 1);
+    CK(cudaMemcpy(ns.data(), ctx->W.nstart, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost));
+    for (int64_t p = 0; p < n; p++)
+      for (uint32_t c = ns[p]; c < ns[p + 1] && c < nrec; c++) fst[c] = (uint32_t)p;
+  }
   if (M || MX) {
     mom.resize(nrec);
     CK(cudaMemcpy(mom.data(), ctx->W.rec_mom, (size_t)nrec * 32, cudaMemcpyDeviceToHost));

@@ -16,10 +16,13 @@
 //                       rec[c].aux uint4  (T_acc, T_rej, skip, meta) 16 B
 //                       (one 32-byte sector per record: a lane's visit
 //                       touches one sector)
-//                       rec_first[c] u32 first sorted particle  (export)
 //                       rec_mom[c] double4 (M, MX, MY, MZ) fp64 (internal)
 //                     skip(c) = index of the first record after c's subtree,
 //                     so DFS next = c + 1 and "accept" jumps to skip(c).
+//                     Particle p's records are [nstart[p], nstart[p+1]).
+//   level items     : per level 0..22, the records of that level in Morton
+//                     order (item_rec, item_clo, lvl_skip, lvl_mom; tree.cu),
+//                     so K5 streams each node's children.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -27,6 +30,7 @@
 #include "../../include/bh.h"
 
 #define BH_MAXLEVEL 21
+#define BH_NLEVELS 23  // item levels 0 .. 22 (22: bucket members)
 #define BH_NPHASE 6
 
 namespace bh {
@@ -38,6 +42,7 @@ enum : uint32_t {
   META_MEMBER = 1u << 6,   // bucket member record (not a tree node of the export)
   META_BUCKET = 1u << 7,   // level-21 node with >= 2 particles
 };
+#define ITEM_LEAF 0x80000000u  // item_rec flag: the item is a particle's own record
 
 // device status block (one per ctx, in the workspace)
 enum : uint32_t {
@@ -67,9 +72,8 @@ struct DevStatus {
   float L;
   float scale;
   uint32_t pad[3];
-  uint32_t lvl_count[24];   // internal nodes per level (0..21)
-  uint32_t lvl_offset[24];  // exclusive prefix of lvl_count
-  uint32_t lvl_cursor[24];
+  uint32_t lvl_count[24];   // items (records) per level 0..22; [23] = 0
+  uint32_t lvl_offset[24];  // exclusive prefix of lvl_count (level-ordered item arrays)
   // walk statistics per record level (stats mode): group iterations, active
   // lane-visits, interactions
   unsigned long long lvl_iters[24];
@@ -121,14 +125,19 @@ struct Workspace {
   ResumeState *resume;  // cap_resume entries (queue slots beyond it re-walk from the root)
   int64_t cap_resume;
   int resume_stack;     // 0: the full resume LIFO; > 0: a smaller one (test hook)
-  uint32_t *rec_first;
   double4 *rec_mom;
-  uint32_t *lvl_list;
+  // level-ordered items (tree.cu): per level, the records in Morton order
+  uint32_t *blkcnt;     // [23][blocks of 256 particles]: item counts, then offsets
+  uint32_t *item_rec;   // record index | ITEM_LEAF
+  uint32_t *item_clo;   // items of the next level whose first particle precedes this one's
+  uint32_t *lvl_skip;   // skip() of the item's record
+  double4 *lvl_mom;     // fp64 (M, MX, MY, MZ) of the item
+  double *lvl_q;        // multipole = 2: fp64 quadrupole of the item (6 per item; null otherwise)
   DevStatus *status;
 };
 
 struct Layout {
-  int64_t n, cap_rec, cap_int, n_own_max, sort_tiles, scan_tiles, cap_resume;
+  int64_t n, cap_rec, cap_int, n_own_max, sort_tiles, scan_tiles, cap_resume, blocks;
   size_t total;
   size_t off[32];
 };
@@ -158,8 +167,7 @@ cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s);
 cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s);
 cudaError_t launch_tie_fixup(const Workspace &W, int64_t n, int buf, cudaStream_t s);
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, cudaStream_t s);
-cudaError_t launch_moments(const Workspace &W, int64_t n, int64_t cap_rec, int64_t cap_int, double theta,
-                           cudaStream_t s, int *launches);
+cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, cudaStream_t s, int *launches);
 cudaError_t launch_scan_u32(uint32_t *data, int64_t count, uint32_t *tmp, cudaStream_t s);
 cudaError_t launch_own_targets(const Workspace &W, int64_t n, int buf, uint32_t own_lo, uint32_t own_hi,
                                cudaStream_t s);

@@ -9,10 +9,12 @@
 // operation is an explicit round-to-nearest intrinsic, so the result is
 // bit-identical to the oracle's recursive sums.
 //
-// One launch per level l = 21 .. 0 over that level's node list (K4 built the
-// lists); a node reads its children's records, which the previous launch (or
-// K4, for particle records) wrote.  The kernel also emits each node's fp32 walk
-// record: com32 = RN(com), M32 = RN(M), and the two fp32 thresholds of the
+// One launch per level l = 21 .. 0 over that level's Morton-ordered items (K4,
+// tree.cu): an internal node's children are the contiguous range
+// [clo(node), clo(next item)) of the level-(l+1) items, whose fp64 moments the
+// previous launch (or K4, for particles: (m, m x)) wrote in level order, so
+// the sums stream.  skip() comes bottom-up too (the last child's).  The kernel
+// also emits each node's fp32 walk record: com32 = RN(com), M32 = RN(M), and the two fp32 thresholds of the
 // force walk's MAC filter (walk.cu):
 //   accept for sure  if d2_32 > T_acc,   open for sure  if d2_32 < T_rej,
 //   otherwise the walk re-evaluates the exact fp64 test of the oracle.
@@ -54,70 +56,68 @@ __device__ __forceinline__ void add_point_quad(double Q[6], double m, double y0,
   Q[5] = __dadd_rn(Q[5], __dmul_rn(m, __dmul_rn(__dmul_rn(3.0, y1), y2)));
 }
 
-__global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatus *__restrict__ st,
-                                                       const uint32_t *__restrict__ lvl_list,
-                                                       Rec *__restrict__ rec,
-                                                       double4 *__restrict__ rec_mom, double theta,
-                                                       double *__restrict__ qmom, float4 *__restrict__ qrec) {
-  if (st->err & ERR_NODE_OVERFLOW) return;
-  const uint32_t cnt = st->lvl_count[level];
-  const uint32_t off = st->lvl_offset[level];
-  const double Ld = (double)st->L;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
-    const uint32_t c = lvl_list[off + t];
-    const uint4 aux = rec[c].aux;
-    const uint32_t end = aux.z;
+template <bool QUAD>
+__device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, uint32_t lo, uint32_t hi, uint32_t off,
+                                             uint32_t off1, double Ld, double theta,
+                                             const uint32_t *__restrict__ item_rec, uint32_t *__restrict__ lvl_skip,
+                                             double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
+                                             double4 *__restrict__ rec_mom, double *__restrict__ lvl_q,
+                                             double *__restrict__ qmom, float4 *__restrict__ qrec) {
+  {
+    const uint32_t skip = lvl_skip[off1 + hi - 1];  // the last child's
+    // the children in digit order (reading L14): a particle contributes
+    // (m, m x), an internal node its (M, MX); the first four are loaded at once
+    double4 q[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) q[k] = lo + k < hi ? lvl_mom[off1 + lo + k] : make_double4(0.0, 0.0, 0.0, 0.0);
     double M = 0.0, X = 0.0, Y = 0.0, Z = 0.0;
-    uint32_t ch = c + 1;
-    while (ch < end) {
-      uint4 ca = rec[ch].aux;
-      if (ca.w & META_LEAF) {
-        float4 p = rec[ch].cm;
-        double m = (double)p.w;
-        M = __dadd_rn(M, m);
-        X = __dadd_rn(X, __dmul_rn(m, (double)p.x));
-        Y = __dadd_rn(Y, __dmul_rn(m, (double)p.y));
-        Z = __dadd_rn(Z, __dmul_rn(m, (double)p.z));
-        ch = ch + 1;
-      } else {
-        double4 q = rec_mom[ch];
-        M = __dadd_rn(M, q.x);
-        X = __dadd_rn(X, q.y);
-        Y = __dadd_rn(Y, q.z);
-        Z = __dadd_rn(Z, q.w);
-        ch = ca.z;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if (lo + k < hi) {
+        M = __dadd_rn(M, q[k].x);
+        X = __dadd_rn(X, q[k].y);
+        Y = __dadd_rn(Y, q[k].z);
+        Z = __dadd_rn(Z, q[k].w);
       }
     }
+    for (uint32_t j = lo + 4; j < hi; j++) {
+      const double4 r = lvl_mom[off1 + j];
+      M = __dadd_rn(M, r.x);
+      X = __dadd_rn(X, r.y);
+      Y = __dadd_rn(Y, r.z);
+      Z = __dadd_rn(Z, r.w);
+    }
+    lvl_mom[off + t] = make_double4(M, X, Y, Z);
+    lvl_skip[off + t] = skip;
     rec_mom[c] = make_double4(M, X, Y, Z);
     const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
     const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
-    rec[c].cm = make_float4(fx, fy, fz, __double2float_rn(M));
-    if (qmom) {
+    if (QUAD) {
       // the quadrupole about (cx, cy, cz): the children in digit order, each its
       // own Q plus its mass at its com's offset (parallel-axis rule)
       double Q[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      uint32_t q = c + 1;
-      while (q < end) {
-        const uint4 ca = rec[q].aux;
-        if (ca.w & META_LEAF) {
-          const float4 pp = rec[q].cm;
+      for (uint32_t j = lo; j < hi; j++) {
+        const uint32_t ec = item_rec[off1 + j];
+        if (ec & ITEM_LEAF) {
+          const float4 pp = rec[ec & ~ITEM_LEAF].cm;
           add_point_quad(Q, (double)pp.w, __dsub_rn((double)pp.x, cx), __dsub_rn((double)pp.y, cy),
                          __dsub_rn((double)pp.z, cz));
-          q = q + 1;
         } else {
-          const double *qc = qmom + 6 * (size_t)q;
+          const double *qc = lvl_q + 6 * (size_t)(off1 + j);
 #pragma unroll
           for (int k = 0; k < 6; k++) Q[k] = __dadd_rn(Q[k], qc[k]);
-          const double4 mc = rec_mom[q];
+          const double4 mc = lvl_mom[off1 + j];
           add_point_quad(Q, mc.x, __dsub_rn(__ddiv_rn(mc.y, mc.x), cx), __dsub_rn(__ddiv_rn(mc.z, mc.x), cy),
                          __dsub_rn(__ddiv_rn(mc.w, mc.x), cz));
-          q = ca.z;
         }
       }
 #pragma unroll
-      for (int k = 0; k < 6; k++) qmom[6 * (size_t)c + k] = Q[k];
-      // the walk's copy is -Q in fp32 (walk.cu quad_pair: the minus sign of the
-      // field's first term rides on Q, exactly)
+      for (int k = 0; k < 6; k++) {
+        qmom[6 * (size_t)c + k] = Q[k];
+        lvl_q[6 * (size_t)(off + t) + k] = Q[k];
+      }
+      // the walk's copy is -Q in fp32 (walk.cu: the minus sign of the field's
+      // first term rides on Q, exactly)
       qrec[2 * (size_t)c] = make_float4(-__double2float_rn(Q[0]), -__double2float_rn(Q[1]),
                                         -__double2float_rn(Q[2]), -__double2float_rn(Q[3]));
       qrec[2 * (size_t)c + 1] = make_float4(-__double2float_rn(Q[4]), -__double2float_rn(Q[5]), 0.f, 0.f);
@@ -147,21 +147,74 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
       // re-walk, which tests containment.
       if (level >= 20) tacc = INFINITY;
     }
-    rec[c].aux = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), aux.z, aux.w);
+    Rec r;
+    r.cm = make_float4(fx, fy, fz, __double2float_rn(M));
+    r.aux = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), skip,
+                       (uint32_t)level | (level == BH_MAXLEVEL ? META_BUCKET : 0u));
+    rec[c] = r;
   }
 }
 
-cudaError_t launch_moments(const Workspace &W, int64_t n, int64_t cap_rec, int64_t cap_int, double theta,
-                           cudaStream_t s, int *launches) {
-  (void)cap_rec;
-  // grid: enough blocks for the widest level, capped at 8 waves of 148 SMs
-  int64_t need = (cap_int + 255) / 256;
+template <bool QUAD>
+__global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatus *__restrict__ st,
+                                                       const uint32_t *__restrict__ item_rec,
+                                                       const uint32_t *__restrict__ item_clo,
+                                                       uint32_t *__restrict__ lvl_skip,
+                                                       double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
+                                                       double4 *__restrict__ rec_mom, double theta,
+                                                       double *__restrict__ lvl_q, double *__restrict__ qmom,
+                                                       float4 *__restrict__ qrec) {
+  if (st->err & ERR_NODE_OVERFLOW) return;
+  const uint32_t cnt = st->lvl_count[level];
+  const uint32_t off = st->lvl_offset[level];
+  const uint32_t cnt1 = st->lvl_count[level + 1];
+  const uint32_t off1 = st->lvl_offset[level + 1];
+  const double Ld = (double)st->L;
+  // one round trip for an item, one for its children (loads hoisted so they
+  // are in flight together); the next item's loads are issued before this
+  // one's children are summed
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t e = ITEM_LEAF, lo = 0, hi = 0;
+  if (t < cnt) {
+    e = item_rec[off + t];
+    lo = item_clo[off + t];
+    hi = t + 1 < cnt ? item_clo[off + t + 1] : cnt1;
+  }
+  for (; t < cnt; t += stride) {
+    const uint32_t tn = t + stride;
+    uint32_t en = ITEM_LEAF, lon = 0, hin = 0;
+    if (tn < cnt) {
+      en = item_rec[off + tn];
+      lon = item_clo[off + tn];
+      hin = tn + 1 < cnt ? item_clo[off + tn + 1] : cnt1;
+    }
+    const uint32_t ecur = e, locur = lo, hicur = hi;
+    e = en;
+    lo = lon;
+    hi = hin;
+    if (ecur & ITEM_LEAF) continue;  // a particle: K4 wrote its record and moments
+    moments_node<QUAD>(level, t, ecur, locur, hicur, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec, rec_mom,
+                       lvl_q, qmom, qrec);
+  }
+}
+
+
+cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, cudaStream_t s, int *launches) {
   if (n < 2) return cudaSuccess;
+  // grid: enough blocks for the widest level (at most n items), capped at 8
+  // waves of 148 SMs
+  int64_t need = (n + 255) / 256;
   int64_t lim = 148 * 8;
   int grid = (int)(need < lim ? need : lim);
   if (grid < 1) grid = 1;
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
-    k_moments_level<<<grid, 256, 0, s>>>(l, W.status, W.lvl_list, W.rec, W.rec_mom, theta, W.qmom, W.qrec);
+    if (W.qmom)
+      k_moments_level<true><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom, W.rec,
+                                                 W.rec_mom, theta, W.lvl_q, W.qmom, W.qrec);
+    else
+      k_moments_level<false><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom,
+                                                  W.rec, W.rec_mom, theta, W.lvl_q, W.qmom, W.qrec);
     if (launches) (*launches)++;
   }
   return cudaGetLastError();

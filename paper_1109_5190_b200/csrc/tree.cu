@@ -16,12 +16,22 @@
 //   DFS pre-order == lexicographic (first particle, level), so the records of
 //   particle p occupy [nstart[p], nstart[p+1]) with nstart = exclusive scan of
 //   (max(0, b - a) + 1), and skip(node) = nstart[last particle + 1].
-// The last particle of a level-l node starting at p is found by galloping /
-// binary search on the key prefix (deepest level first, each search starting
-// at the previous end), O(log count) per node.
+// Level-ordered items.  Every record is one "item" of its level: the internal
+// nodes of particle p at levels a+1 .. b and its leaf at max(a, b) + 1 (22 for
+// a bucket member), all with first particle p.  K4 also lists each level's
+// items in Morton order (item_rec: record index | ITEM_LEAF) with, per item,
+// clo = the number of items of the next level whose first particle precedes
+// its own.  The children of an internal node at level l are then exactly the
+// level-(l+1) items [clo(node), clo(next item of level l)) -- one contiguous,
+// Morton-ordered range -- which K5 streams (com.cu); K5 also derives skip()
+// bottom-up (skip of a node = skip of its last child), so K4 does no search.
+// Ranks: per-block item counts per level (k_lcp_count), an exclusive scan per
+// level over the blocks (k_level_scan), in-block ranks by warp ballots (k_emit).
 //
 // HBM: ~3 key reads (8 B, mostly cached) + 1 B lcp + scan traffic + record
-// writes (16 + 16 + 4 B per record) + a 16 B gather of the particle per leaf.
+// writes (leaf 32 B, internal nodes 4 B here, the rest in K5) + 8 B of item
+// lists per record + a 16 B gather of the particle and 36 B of level-ordered
+// moments per leaf.
 #include "bh_internal.cuh"
 
 namespace bh {
@@ -32,14 +42,16 @@ __device__ __forceinline__ int shared_digits(unsigned long long a, unsigned long
   return (__clzll(x) - 1) / 3;  // keys are 63-bit: bit 63 is always 0
 }
 
-// L_p, record counts n_p and the per-level histogram of internal nodes
+// L_p, record counts n_p and the per-block item counts of every level
+// (blkcnt[level][block], levels 0 .. 22)
 __global__ void __launch_bounds__(256) k_lcp_count(const unsigned long long *__restrict__ keys, int64_t n,
                                                    uint8_t *__restrict__ lcp, uint32_t *__restrict__ nstart,
-                                                   DevStatus *st) {
-  __shared__ uint32_t lh[24];
-  if (threadIdx.x < 24) lh[threadIdx.x] = 0;
+                                                   uint32_t *__restrict__ blkcnt, int64_t nblk) {
+  __shared__ uint32_t lh[BH_NLEVELS];
+  if (threadIdx.x < BH_NLEVELS) lh[threadIdx.x] = 0;
   __syncthreads();
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int lo = BH_NLEVELS, ll = -1;  // this particle's item levels (none past n)
   if (p < n) {
     unsigned long long kp = keys[p];
     int a = p > 0 ? shared_digits(keys[p - 1], kp) : -1;
@@ -47,28 +59,102 @@ __global__ void __launch_bounds__(256) k_lcp_count(const unsigned long long *__r
     if (p + 1 < n) lcp[p] = (uint8_t)b;
     int ni = b > a ? b - a : 0;
     nstart[p] = (uint32_t)ni + 1u;
-    for (int l = a + 1; l <= b; l++) atomicAdd(&lh[l], 1u);
+    ll = (a > b ? a : b) + 1;  // leaf level (22: bucket member)
+    lo = a + 1;
   }
   if (p == n) nstart[n] = 0;
+  for (int l = lo; l <= ll; l++) atomicAdd(&lh[l], 1u);  // items of levels lo .. ll
   __syncthreads();
-  if (threadIdx.x < 22 && lh[threadIdx.x]) atomicAdd(&st->lvl_count[threadIdx.x], lh[threadIdx.x]);
+  if (threadIdx.x < BH_NLEVELS) blkcnt[threadIdx.x * nblk + blockIdx.x] = lh[threadIdx.x];
 }
 
-// tiny: level offsets, capacity check
-__global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, int64_t cap_rec, int64_t cap_int,
-                              DevStatus *st, Rec *__restrict__ rec, float4 *__restrict__ qrec) {
+// Per-level exclusive scan of the per-block counts in two passes:
+// k_level_scan_seg: segments of LS_SEG blocks, one thread block each (grid
+// segments x levels): local exclusive scan in place + the segment totals;
+// k_level_scan_top: one thread block per level scans the segment totals in
+// place (-> segment offsets) and writes the level's item count.
+// Global rank base of particle block k at level l: blkcnt[l][k] + segsum[l][k / LS_SEG].
+constexpr int LS_SEG = 1024;
+__global__ void __launch_bounds__(256) k_level_scan_seg(uint32_t *__restrict__ blkcnt, int64_t nblk,
+                                                        uint32_t *__restrict__ segsum, int64_t nseg) {
+  __shared__ uint32_t wsum[8];
+  const int l = blockIdx.y;
+  uint32_t *col = blkcnt + l * nblk + (int64_t)blockIdx.x * LS_SEG;
+  const int64_t len = nblk - (int64_t)blockIdx.x * LS_SEG < LS_SEG ? nblk - (int64_t)blockIdx.x * LS_SEG : LS_SEG;
+  uint32_t v[4], sum = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const int64_t i = threadIdx.x * 4 + k;
+    v[k] = i < len ? col[i] : 0u;
+    sum += v[k];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  uint32_t run = x - sum;
+  for (int k = 0; k < w; k++) run += wsum[k];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const int64_t i = threadIdx.x * 4 + k;
+    if (i < len) col[i] = run;
+    run += v[k];
+  }
+  if (threadIdx.x == 255) segsum[l * nseg + blockIdx.x] = run;
+}
+
+__global__ void __launch_bounds__(1024) k_level_scan_top(uint32_t *__restrict__ segsum, int64_t nseg, DevStatus *st) {
+  __shared__ uint32_t wsum[32];
+  uint32_t *col = segsum + blockIdx.x * nseg;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t carry = 0;
+  for (int64_t base = 0; base < nseg; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t v = i < nseg ? col[i] : 0u;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t t = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    if (i < nseg) col[i] = carry + x - v + (w > 0 ? wsum[w - 1] : 0u);
+    carry += wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) st->lvl_count[blockIdx.x] = carry;
+}
+
+// tiny: level offsets, capacity check, the walk's sentinel record
+__global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, int64_t cap_rec, DevStatus *st,
+                              Rec *__restrict__ rec, float4 *__restrict__ qrec) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint32_t run = 0;
-  for (int l = 0; l < 24; l++) {
+  for (int l = 0; l < BH_NLEVELS; l++) {
     st->lvl_offset[l] = run;
-    st->lvl_cursor[l] = run;
     run += st->lvl_count[l];
   }
-  st->n_internal = run;
+  st->lvl_offset[BH_NLEVELS] = run;
+  st->lvl_count[BH_NLEVELS] = 0;
   uint32_t nrec = nstart[n];
   st->n_records = nrec;
-  // one extra slot for the walk's sentinel record (walk.cu k_walk2)
-  if ((int64_t)nrec + 1 > cap_rec || (int64_t)run > cap_int) {
+  st->n_internal = nrec - (uint32_t)n;
+  // one extra slot for the walk's sentinel record (walk.cu k_walk2); every
+  // record is one item
+  if ((int64_t)nrec + 1 > cap_rec || run != nrec) {
     st->err |= ERR_NODE_OVERFLOW;
     return;
   }
@@ -80,68 +166,89 @@ __global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, in
   }
 }
 
-// last index q >= start with (keys[q] >> sh) == prefix, given keys[start] matches
-__device__ __forceinline__ int64_t run_end(const unsigned long long *__restrict__ keys, int64_t n, int64_t start,
-                                           int sh, unsigned long long prefix) {
-  int64_t lo = start, step = 1, hi;
-  for (;;) {
-    int64_t probe = lo + step;
-    if (probe >= n) { hi = n; break; }
-    if ((keys[probe] >> sh) != prefix) { hi = probe; break; }
-    lo = probe;
-    step <<= 1;
-  }
-  // keys[lo] matches, hi is n or a non-match
-  while (hi - lo > 1) {
-    int64_t mid = lo + ((hi - lo) >> 1);
-    if ((keys[mid] >> sh) == prefix) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
+// Records and level-ordered item lists.  Internal nodes get their record in
+// K5; a particle's leaf record is complete here
+// (com = the particle, T_acc = -inf, skip = c + 1) and its level-ordered
+// moments are (m, m x, m y, m z) in fp64 (exact).
 __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restrict__ keys,
                                               const uint32_t *__restrict__ vals, const uint8_t *__restrict__ lcp,
                                               const uint32_t *__restrict__ nstart, const float4 *__restrict__ pos4,
                                               int64_t n, DevStatus *st, Rec *__restrict__ rec,
-                                              uint32_t *__restrict__ rec_first,
-                                              uint32_t *__restrict__ lvl_list, float4 *__restrict__ qrec) {
-  __shared__ uint32_t cnt[24], slot[24], gb[24];
+                                              const uint32_t *__restrict__ blkoff,
+                                              int64_t nblk, const uint32_t *__restrict__ segoff, int64_t nseg,
+                                              uint32_t *__restrict__ item_rec,
+                                              uint32_t *__restrict__ item_clo, uint32_t *__restrict__ lvl_skip,
+                                              double4 *__restrict__ lvl_mom, float4 *__restrict__ qrec) {
+  __shared__ uint16_t s_pre[BH_NLEVELS][256];
+  __shared__ uint32_t s_w[BH_NLEVELS][8];
+  __shared__ uint32_t s_off[BH_NLEVELS + 1];
   if (st->err & ERR_NODE_OVERFLOW) return;  // uniform: nothing safe to write
-  if (threadIdx.x < 24) { cnt[threadIdx.x] = 0; slot[threadIdx.x] = 0; }
-  __syncthreads();
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  (void)keys;
+  for (int i = threadIdx.x; i < BH_NLEVELS * 8; i += blockDim.x) (&s_w[0][0])[i] = 0u;
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int a = -1, b = -1;
   if (p < n) {
     a = p > 0 ? (int)lcp[p - 1] : -1;
     b = p + 1 < n ? (int)lcp[p] : -1;
-    for (int l = a + 1; l <= b; l++) atomicAdd(&cnt[l], 1u);
+  }
+  const int ll = (a > b ? a : b) + 1;  // leaf level
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  if (threadIdx.x < BH_NLEVELS) s_off[threadIdx.x] = st->lvl_offset[threadIdx.x];
+  __syncthreads();
+  // in-block exclusive item ranks per level, over the levels this warp needs
+  // (a+1 .. leaf level + 1: the items and their clo)
+  const int wlo = __reduce_min_sync(0xffffffffu, p < n ? a + 1 : BH_NLEVELS);
+  const int whi = __reduce_max_sync(0xffffffffu, p < n ? (ll + 1 < BH_NLEVELS ? ll + 1 : BH_NLEVELS - 1) : -1);
+  for (int l = wlo; l <= whi; l++) {
+    const bool has = p < n && l > a && l <= ll;
+    const uint32_t bal = __ballot_sync(0xffffffffu, has);
+    s_pre[l][threadIdx.x] = (uint16_t)__popc(bal & lt);
+    if (lane == 0) s_w[l][w] = __popc(bal);
   }
   __syncthreads();
-  if (threadIdx.x < 22 && cnt[threadIdx.x]) gb[threadIdx.x] = atomicAdd(&st->lvl_cursor[threadIdx.x], cnt[threadIdx.x]);
+  if (threadIdx.x < BH_NLEVELS) {  // exclusive over the block's warps
+    uint32_t run = 0;
+    for (int k = 0; k < 8; k++) {
+      const uint32_t c = s_w[threadIdx.x][k];
+      s_w[threadIdx.x][k] = run;
+      run += c;
+    }
+  }
   __syncthreads();
   if (p >= n) return;
+  // global rank of this particle's item at level l (the count of level-l
+  // items with first particle < p), l <= 22; 0 past the last level
+  auto rank = [&](int l) -> uint32_t {
+    if (l >= BH_NLEVELS) return 0u;
+    return blkoff[l * nblk + blockIdx.x] + segoff[l * nseg + blockIdx.x / LS_SEG] + s_pre[l][threadIdx.x] + s_w[l][w];
+  };
   const uint32_t base = nstart[p];
-  const unsigned long long kp = keys[p];
-  int64_t e = p + 1;  // deepest internal node holds at least p and p+1
-  for (int l = b; l > a; l--) {
-    int sh = 3 * (BH_MAXLEVEL - l);
-    e = run_end(keys, n, e, sh, kp >> sh);
-    uint32_t c = base + (uint32_t)(l - a - 1);
-    uint32_t skip = nstart[e + 1];
-    rec_first[c] = (uint32_t)p;
-    uint32_t meta = (uint32_t)l | (l == BH_MAXLEVEL ? META_BUCKET : 0u);
-    rec[c].aux = make_uint4(0u, 0u, skip, meta);
-    uint32_t s = atomicAdd(&slot[l], 1u);
-    lvl_list[gb[l] + s] = c;
+  uint32_t rk = rank(a + 1);
+  for (int l = a + 1; l <= b; l++) {  // internal nodes at levels a+1 .. b
+    const uint32_t c = base + (uint32_t)(l - a - 1);
+    const uint32_t rn = rank(l + 1);
+    item_rec[s_off[l] + rk] = c;
+    item_clo[s_off[l] + rk] = rn;
+    rk = rn;
   }
-  int top = a > b ? a : b;
-  uint32_t c = base + (uint32_t)(b > a ? b - a : 0);
-  uint32_t meta = top + 1 <= BH_MAXLEVEL ? ((uint32_t)(top + 1) | META_LEAF)
-                                         : ((uint32_t)(BH_MAXLEVEL + 1) | META_LEAF | META_MEMBER);
-  rec_first[c] = (uint32_t)p;
-  rec[c].cm = pos4[vals[p]];
+  // the particle's own record: a leaf at level ll (<= 21) or a bucket member (22)
+  const uint32_t c = base + (uint32_t)(b > a ? b - a : 0);
+  const uint32_t meta = ll <= BH_MAXLEVEL ? ((uint32_t)ll | META_LEAF)
+                                          : ((uint32_t)(BH_MAXLEVEL + 1) | META_LEAF | META_MEMBER);
+  const float4 q = pos4[vals[p]];
+  Rec r;
+  r.cm = q;
   // T_acc = -inf: a particle record is always "accepted" unless it is the target
-  rec[c].aux = make_uint4(__float_as_uint(-INFINITY), __float_as_uint(-INFINITY), c + 1u, meta);
+  r.aux = make_uint4(__float_as_uint(-INFINITY), __float_as_uint(-INFINITY), c + 1u, meta);
+  rec[c] = r;
+  const uint32_t k = s_off[ll] + rk;
+  item_rec[k] = c | ITEM_LEAF;
+  item_clo[k] = rank(ll + 1);
+  lvl_skip[k] = c + 1u;
+  const double m = (double)q.w;
+  lvl_mom[k] = make_double4(m, __dmul_rn(m, (double)q.x), __dmul_rn(m, (double)q.y), __dmul_rn(m, (double)q.z));
   if (qrec) {  // multipole = 2: a particle has no quadrupole about itself
     qrec[2 * (size_t)c] = make_float4(0.f, 0.f, 0.f, 0.f);
     qrec[2 * (size_t)c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -149,16 +256,18 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
 }
 
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(W.status->lvl_count, 0, sizeof(uint32_t) * 24 * 3, s);
+  const int64_t nblk = (n + 1 + 255) / 256;
+  k_lcp_count<<<(unsigned)nblk, 256, 0, s>>>(W.keys[buf], n, W.lcp, W.nstart, W.blkcnt, nblk);
+  cudaError_t e = launch_scan_u32(W.nstart, n + 1, W.scan_tmp, s);
   if (e != cudaSuccess) return e;
-  unsigned blocks = (unsigned)((n + 1 + 255) / 256);
-  k_lcp_count<<<blocks, 256, 0, s>>>(W.keys[buf], n, W.lcp, W.nstart, W.status);
-  e = launch_scan_u32(W.nstart, n + 1, W.scan_tmp, s);
-  if (e != cudaSuccess) return e;
-  // cap_int: the level list holds at most cap_rec - n internal nodes
-  k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, cap_rec - n, W.status, W.rec, W.qrec);
+  const int64_t nseg = (nblk + LS_SEG - 1) / LS_SEG;
+  uint32_t *segsum = W.blkcnt + BH_NLEVELS * nblk;
+  k_level_scan_seg<<<dim3((unsigned)nseg, BH_NLEVELS), 256, 0, s>>>(W.blkcnt, nblk, segsum, nseg);
+  k_level_scan_top<<<BH_NLEVELS, 1024, 0, s>>>(segsum, nseg, W.status);
+  k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, W.status, W.rec, W.qrec);
   k_emit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.lcp, W.nstart, W.pos4, n,
-                                                     W.status, W.rec, W.rec_first, W.lvl_list, W.qrec);
+                                                     W.status, W.rec, W.blkcnt, nblk, segsum, nseg, W.item_rec,
+                                                     W.item_clo, W.lvl_skip, W.lvl_mom, W.qrec);
   return cudaGetLastError();
 }
 
