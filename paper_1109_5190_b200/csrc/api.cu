@@ -118,8 +118,8 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
       sizeof(float) * 8 * BBOX_BLOCKS,         // 15 bbox partials
       (size_t)L.cap_rec * 32,                  // 16 rec (cm + aux)
       (size_t)L.cap_resume * sizeof(ResumeState),  // 17 walk resume states
-      0,                                       // 18 (unused)
-      (size_t)L.cap_rec * 32,                  // 19 rec_mom
+      (size_t)L.cap_rec * 4,                   // 18 rec_item: level-item index of each record
+      0,                                       // 19 (unused)
       (size_t)L.cap_rec * 4,                   // 20 item_rec (level-ordered items)
       (size_t)n * 4,                           // 21 redo list
       (size_t)n * 4,                           // 22 walk cost per particle (its group's trips)
@@ -163,7 +163,7 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.rec = (Rec *)(b + L.off[16]);
   W.resume = (ResumeState *)(b + L.off[17]);
   W.cap_resume = L.cap_resume;
-  W.rec_mom = (double4 *)(b + L.off[19]);
+  W.rec_item = (uint32_t *)(b + L.off[18]);
   W.item_rec = (uint32_t *)(b + L.off[20]);
   W.item_clo = (uint32_t *)(b + L.off[25]);
   W.lvl_skip = (uint32_t *)(b + L.off[26]);
@@ -596,8 +596,8 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
     k_pack<<<blocks_for(n), 256, 0, s>>>(ctx->W.pos4, dp, dm, n);
     k_iota<<<blocks_for(n), 256, 0, s>>>(ctx->W.uid, n);
     if (cudaGetLastError() != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "pack launch failed"); break; }
-    // velocities (user order) parked as float4 in rec_mom (>= 32 B per particle)
-    float4 *vtmp = (float4 *)ctx->W.rec_mom;
+    // velocities (user order) parked as float4 in lvl_mom (>= 32 B per particle)
+    float4 *vtmp = (float4 *)ctx->W.lvl_mom;
     if (dv) {
       k_pack<<<blocks_for(n), 256, 0, s>>>(vtmp, dv, dm, n);  // .w = mass, ignored
     }
@@ -877,7 +877,12 @@ static bh_status export_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint3
   }
   if (M || MX) {
     mom.resize(nrec);
-    CK(cudaMemcpy(mom.data(), ctx->W.rec_mom, (size_t)nrec * 32, cudaMemcpyDeviceToHost));
+    // fp64 moments: the level-ordered item of each record
+    std::vector<uint32_t> item(nrec);
+    std::vector<double4> lm(nrec);
+    CK(cudaMemcpy(item.data(), ctx->W.rec_item, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(lm.data(), ctx->W.lvl_mom, (size_t)nrec * 32, cudaMemcpyDeviceToHost));
+    for (uint32_t c = 0; c < nrec; c++) mom[c] = lm[item[c]];
   }
   int64_t k = 0;
   for (uint32_t c = 0; c < nrec; c++) {

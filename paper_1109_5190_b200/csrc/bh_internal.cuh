@@ -16,13 +16,13 @@
 //                       rec[c].aux uint4  (T_acc, T_rej, skip, meta) 16 B
 //                       (one 32-byte sector per record: a lane's visit
 //                       touches one sector)
-//                       rec_mom[c] double4 (M, MX, MY, MZ) fp64 (internal)
 //                     skip(c) = index of the first record after c's subtree,
 //                     so DFS next = c + 1 and "accept" jumps to skip(c).
 //                     Particle p's records are [nstart[p], nstart[p+1]).
 //   level items     : per level 0..22, the records of that level in Morton
 //                     order (item_rec, item_clo, lvl_skip, lvl_mom; tree.cu),
-//                     so K5 streams each node's children.
+//                     so K5 streams each node's children; rec_item[c] maps a
+//                     record to its item (fp64 moments of record c = lvl_mom[rec_item[c]]).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -125,7 +125,7 @@ struct Workspace {
   ResumeState *resume;  // cap_resume entries (queue slots beyond it re-walk from the root)
   int64_t cap_resume;
   int resume_stack;     // 0: the full resume LIFO; > 0: a smaller one (test hook)
-  double4 *rec_mom;
+  uint32_t *rec_item;   // per record: its index in the level-ordered item arrays
   // level-ordered items (tree.cu): per level, the records in Morton order
   uint32_t *blkcnt;     // [23][blocks of 256 particles]: item counts, then offsets
   uint32_t *item_rec;   // record index | ITEM_LEAF

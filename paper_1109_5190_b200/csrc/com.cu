@@ -30,6 +30,18 @@
 
 #include "bh_internal.cuh"
 
+#ifndef BH_MOM_PREFETCH
+#define BH_MOM_PREFETCH 4
+#endif
+#ifndef BH_MOM_MINB
+#define BH_MOM_MINB 0  // 0: no minimum-blocks bound
+#endif
+#if BH_MOM_MINB > 0
+#define BH_MOM_BOUNDS __launch_bounds__(256, BH_MOM_MINB)
+#else
+#define BH_MOM_BOUNDS __launch_bounds__(256)
+#endif
+
 namespace bh {
 
 __device__ __forceinline__ float round_up_f(double x) {
@@ -61,18 +73,20 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
                                              uint32_t off1, double Ld, double theta,
                                              const uint32_t *__restrict__ item_rec, uint32_t *__restrict__ lvl_skip,
                                              double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
-                                             double4 *__restrict__ rec_mom, double *__restrict__ lvl_q,
+                                             double *__restrict__ lvl_q,
                                              double *__restrict__ qmom, float4 *__restrict__ qrec) {
   {
     const uint32_t skip = lvl_skip[off1 + hi - 1];  // the last child's
     // the children in digit order (reading L14): a particle contributes
-    // (m, m x), an internal node its (M, MX); the first four are loaded at once
-    double4 q[4];
+    // (m, m x), an internal node its (M, MX); the first BH_MOM_PREFETCH are
+    // loaded at once
+    double4 q[BH_MOM_PREFETCH];
 #pragma unroll
-    for (int k = 0; k < 4; k++) q[k] = lo + k < hi ? lvl_mom[off1 + lo + k] : make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int k = 0; k < BH_MOM_PREFETCH; k++)
+      q[k] = lo + k < hi ? lvl_mom[off1 + lo + k] : make_double4(0.0, 0.0, 0.0, 0.0);
     double M = 0.0, X = 0.0, Y = 0.0, Z = 0.0;
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
+    for (int k = 0; k < BH_MOM_PREFETCH; k++) {
       if (lo + k < hi) {
         M = __dadd_rn(M, q[k].x);
         X = __dadd_rn(X, q[k].y);
@@ -80,7 +94,7 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
         Z = __dadd_rn(Z, q[k].w);
       }
     }
-    for (uint32_t j = lo + 4; j < hi; j++) {
+    for (uint32_t j = lo + BH_MOM_PREFETCH; j < hi; j++) {
       const double4 r = lvl_mom[off1 + j];
       M = __dadd_rn(M, r.x);
       X = __dadd_rn(X, r.y);
@@ -89,7 +103,6 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     }
     lvl_mom[off + t] = make_double4(M, X, Y, Z);
     lvl_skip[off + t] = skip;
-    rec_mom[c] = make_double4(M, X, Y, Z);
     const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
     const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
     if (QUAD) {
@@ -156,12 +169,12 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
 }
 
 template <bool QUAD>
-__global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatus *__restrict__ st,
+__global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__restrict__ st,
                                                        const uint32_t *__restrict__ item_rec,
                                                        const uint32_t *__restrict__ item_clo,
                                                        uint32_t *__restrict__ lvl_skip,
                                                        double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
-                                                       double4 *__restrict__ rec_mom, double theta,
+                                                       double theta,
                                                        double *__restrict__ lvl_q, double *__restrict__ qmom,
                                                        float4 *__restrict__ qrec) {
   if (st->err & ERR_NODE_OVERFLOW) return;
@@ -194,7 +207,7 @@ __global__ void __launch_bounds__(256) k_moments_level(int level, const DevStatu
     lo = lon;
     hi = hin;
     if (ecur & ITEM_LEAF) continue;  // a particle: K4 wrote its record and moments
-    moments_node<QUAD>(level, t, ecur, locur, hicur, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec, rec_mom,
+    moments_node<QUAD>(level, t, ecur, locur, hicur, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec,
                        lvl_q, qmom, qrec);
   }
 }
@@ -211,10 +224,10 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, cudaStre
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
     if (W.qmom)
       k_moments_level<true><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom, W.rec,
-                                                 W.rec_mom, theta, W.lvl_q, W.qmom, W.qrec);
+                                                 theta, W.lvl_q, W.qmom, W.qrec);
     else
       k_moments_level<false><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom,
-                                                  W.rec, W.rec_mom, theta, W.lvl_q, W.qmom, W.qrec);
+                                                  W.rec, theta, W.lvl_q, W.qmom, W.qrec);
     if (launches) (*launches)++;
   }
   return cudaGetLastError();

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
                                               int64_t n, DevStatus *st, Rec *__restrict__ rec,
                                               const uint32_t *__restrict__ blkoff,
                                               int64_t nblk, const uint32_t *__restrict__ segoff, int64_t nseg,
-                                              uint32_t *__restrict__ item_rec,
+                                              uint32_t *__restrict__ item_rec, uint32_t *__restrict__ rec_item,
                                               uint32_t *__restrict__ item_clo, uint32_t *__restrict__ lvl_skip,
                                               double4 *__restrict__ lvl_mom, float4 *__restrict__ qrec) {
   __shared__ uint16_t s_pre[BH_NLEVELS][256];
@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
     const uint32_t c = base + (uint32_t)(l - a - 1);
     const uint32_t rn = rank(l + 1);
     item_rec[s_off[l] + rk] = c;
+    rec_item[c] = s_off[l] + rk;
     item_clo[s_off[l] + rk] = rn;
     rk = rn;
   }
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
   rec[c] = r;
   const uint32_t k = s_off[ll] + rk;
   item_rec[k] = c | ITEM_LEAF;
+  rec_item[c] = k;
   item_clo[k] = rank(ll + 1);
   lvl_skip[k] = c + 1u;
   const double m = (double)q.w;
@@ -266,7 +268,7 @@ cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf,
   k_level_scan_top<<<BH_NLEVELS, 1024, 0, s>>>(segsum, nseg, W.status);
   k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, W.status, W.rec, W.qrec);
   k_emit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.lcp, W.nstart, W.pos4, n,
-                                                     W.status, W.rec, W.blkcnt, nblk, segsum, nseg, W.item_rec,
+                                                     W.status, W.rec, W.blkcnt, nblk, segsum, nseg, W.item_rec, W.rec_item,
                                                      W.item_clo, W.lvl_skip, W.lvl_mom, W.qrec);
   return cudaGetLastError();
 }

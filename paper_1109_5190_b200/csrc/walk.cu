@@ -234,7 +234,8 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.rec = W.rec;
   P.quad = a.quad && W.qrec;
   P.qrec = P.quad ? W.qrec : nullptr;
-  P.rec_mom = W.rec_mom;
+  P.lvl_mom = W.lvl_mom;
+  P.rec_item = W.rec_item;
   P.nstart = W.nstart;
   P.vals = W.vals[a.buf];
   P.targets = W.targets;

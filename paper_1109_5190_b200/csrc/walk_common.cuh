@@ -53,7 +53,8 @@ struct WalkParams {
   const Rec *__restrict__ rec;
   const float4 *__restrict__ qrec;  // multipole = 2: -Q (fp32) per record, 2 float4 (else null)
   int quad;
-  const double4 *__restrict__ rec_mom;
+  const double4 *__restrict__ lvl_mom;   // fp64 moments of the level items (exact MAC)
+  const uint32_t *__restrict__ rec_item;  // record -> level item
   const uint32_t *__restrict__ nstart;
   const uint32_t *__restrict__ vals;
   const uint32_t *__restrict__ targets;

@@ -4,10 +4,10 @@
 
 namespace bh {
 
-__device__ __noinline__ bool exact_accept(const double4 *__restrict__ rec_mom, uint32_t c, uint32_t level, float x,
+__device__ __noinline__ bool exact_accept(const double4 *__restrict__ lvl_mom, const uint32_t *__restrict__ rec_item, uint32_t c, uint32_t level, float x,
                                           float y, float z, double L, double theta2) {
   // the oracle's fp64 test (DESIGN.md §3 L4), operation for operation
-  double4 m = rec_mom[c];
+  double4 m = lvl_mom[rec_item[c]];
   double cx = __ddiv_rn(m.y, m.x), cy = __ddiv_rn(m.z, m.x), cz = __ddiv_rn(m.w, m.x);
   double dx = __dsub_rn(cx, (double)x), dy = __dsub_rn(cy, (double)y), dz = __dsub_rn(cz, (double)z);
   double d2 = __dmul_rn(dx, dx);
@@ -48,7 +48,7 @@ __device__ __forceinline__ bool resume_visit(const WalkParams &P, const Target &
   const bool cont = (c <= T.Li) & (au.z > T.Li);
   bool acc = !cont & (d2 > __uint_as_float(au.x));
   if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
-    acc = exact_accept(P.rec_mom, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
+    acc = exact_accept(P.lvl_mom, P.rec_item, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
     A.fb++;
   }
   if (acc) {
