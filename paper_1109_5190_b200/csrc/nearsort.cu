@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long lon
                                                          const uint32_t *__restrict__ tlo, DevStatus *st) {
   if (!st->near_ok) return;
   __shared__ unsigned long long sbad[NM_SMEM], sgood[NS_TILE];
+  __shared__ uint32_t sgval[NS_TILE];  // the good keys' payloads, staged with the keys
   const int64_t nb = st->n_bad, ng = n - nb;
   const unsigned long long *bad = keys1;
   const unsigned long long *good = keys1 + nb;
@@ -119,7 +120,10 @@ __global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long lon
     const int64_t lo = tlo[t], hi = tlo[t + 1];      // bad keys with good[g0] <= k < good[g1]
     const int64_t blo = t == 0 ? 0 : lo;             // tile 0 also takes the bad keys below good[0]
     const bool staged = hi - lo <= NM_SMEM && hi >= lo;
-    for (int64_t i = threadIdx.x; i < gn; i += NS_BLOCK) sgood[i] = good[g0 + i];
+    for (int64_t i = threadIdx.x; i < gn; i += NS_BLOCK) {
+      sgood[i] = good[g0 + i];
+      sgval[i] = vals1[nb + g0 + i];
+    }
     if (staged)
       for (int64_t i = threadIdx.x; i < hi - lo; i += NS_BLOCK) sbad[i] = bad[lo + i];
     __syncthreads();
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(NS_BLOCK) k_near_merge(const unsigned long lon
       }
       const int64_t pos = g0 + i + c;
       keys0[pos] = k;
-      vals0[pos] = vals1[nb + g0 + i];
+      vals0[pos] = sgval[i];
     }
     for (int64_t j = blo + threadIdx.x; j < hi; j += NS_BLOCK) {
       const unsigned long long k = (staged && j >= lo) ? sbad[j - lo] : bad[j];
