@@ -68,6 +68,7 @@ __device__ __forceinline__ void add_point_quad(double Q[6], double m, double y0,
   Q[5] = __dadd_rn(Q[5], __dmul_rn(m, __dmul_rn(__dmul_rn(3.0, y1), y2)));
 }
 
+// one internal node of level `level` at item t (record c, children [lo, hi) of the next level)
 template <bool QUAD>
 __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, uint32_t lo, uint32_t hi, uint32_t off,
                                              uint32_t off1, double Ld, double theta,
@@ -75,97 +76,95 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
                                              double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
                                              double *__restrict__ lvl_q,
                                              double *__restrict__ qmom, float4 *__restrict__ qrec) {
-  {
-    const uint32_t skip = lvl_skip[off1 + hi - 1];  // the last child's
-    // the children in digit order (reading L14): a particle contributes
-    // (m, m x), an internal node its (M, MX); the first BH_MOM_PREFETCH are
-    // loaded at once
-    double4 q[BH_MOM_PREFETCH];
+  const uint32_t skip = lvl_skip[off1 + hi - 1];  // the last child's
+  // the children in digit order (reading L14): a particle contributes
+  // (m, m x), an internal node its (M, MX); the first BH_MOM_PREFETCH are
+  // loaded at once
+  double4 q[BH_MOM_PREFETCH];
 #pragma unroll
-    for (int k = 0; k < BH_MOM_PREFETCH; k++)
-      q[k] = lo + k < hi ? lvl_mom[off1 + lo + k] : make_double4(0.0, 0.0, 0.0, 0.0);
-    double M = 0.0, X = 0.0, Y = 0.0, Z = 0.0;
+  for (int k = 0; k < BH_MOM_PREFETCH; k++)
+    q[k] = lo + k < hi ? lvl_mom[off1 + lo + k] : make_double4(0.0, 0.0, 0.0, 0.0);
+  double M = 0.0, X = 0.0, Y = 0.0, Z = 0.0;
 #pragma unroll
-    for (int k = 0; k < BH_MOM_PREFETCH; k++) {
-      if (lo + k < hi) {
-        M = __dadd_rn(M, q[k].x);
-        X = __dadd_rn(X, q[k].y);
-        Y = __dadd_rn(Y, q[k].z);
-        Z = __dadd_rn(Z, q[k].w);
-      }
+  for (int k = 0; k < BH_MOM_PREFETCH; k++) {
+    if (lo + k < hi) {
+      M = __dadd_rn(M, q[k].x);
+      X = __dadd_rn(X, q[k].y);
+      Y = __dadd_rn(Y, q[k].z);
+      Z = __dadd_rn(Z, q[k].w);
     }
-    for (uint32_t j = lo + BH_MOM_PREFETCH; j < hi; j++) {
-      const double4 r = lvl_mom[off1 + j];
-      M = __dadd_rn(M, r.x);
-      X = __dadd_rn(X, r.y);
-      Y = __dadd_rn(Y, r.z);
-      Z = __dadd_rn(Z, r.w);
-    }
-    lvl_mom[off + t] = make_double4(M, X, Y, Z);
-    lvl_skip[off + t] = skip;
-    const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
-    const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
-    if (QUAD) {
-      // the quadrupole about (cx, cy, cz): the children in digit order, each its
-      // own Q plus its mass at its com's offset (parallel-axis rule)
-      double Q[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      for (uint32_t j = lo; j < hi; j++) {
-        const uint32_t ec = item_rec[off1 + j];
-        if (ec & ITEM_LEAF) {
-          const float4 pp = rec[ec & ~ITEM_LEAF].cm;
-          add_point_quad(Q, (double)pp.w, __dsub_rn((double)pp.x, cx), __dsub_rn((double)pp.y, cy),
-                         __dsub_rn((double)pp.z, cz));
-        } else {
-          const double *qc = lvl_q + 6 * (size_t)(off1 + j);
-#pragma unroll
-          for (int k = 0; k < 6; k++) Q[k] = __dadd_rn(Q[k], qc[k]);
-          const double4 mc = lvl_mom[off1 + j];
-          add_point_quad(Q, mc.x, __dsub_rn(__ddiv_rn(mc.y, mc.x), cx), __dsub_rn(__ddiv_rn(mc.z, mc.x), cy),
-                         __dsub_rn(__ddiv_rn(mc.w, mc.x), cz));
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 6; k++) {
-        qmom[6 * (size_t)c + k] = Q[k];
-        lvl_q[6 * (size_t)(off + t) + k] = Q[k];
-      }
-      // the walk's copy is -Q in fp32 (walk.cu: the minus sign of the field's
-      // first term rides on Q, exactly)
-      qrec[2 * (size_t)c] = make_float4(-__double2float_rn(Q[0]), -__double2float_rn(Q[1]),
-                                        -__double2float_rn(Q[2]), -__double2float_rn(Q[3]));
-      qrec[2 * (size_t)c + 1] = make_float4(-__double2float_rn(Q[4]), -__double2float_rn(Q[5]), 0.f, 0.f);
-    }
-    float tacc, trej;
-    if (!(theta > 0.0)) {
-      tacc = INFINITY;
-      trej = INFINITY;
-    } else {
-      const double u = 5.9604644775390625e-08;  // 2^-24
-      const double s = ldexp(Ld, -level);
-      const double r = s / theta;
-      const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
-      // first-order bounds (u: com rounding |c32 - c64| <= u(1+u)|c32|, one
-      // rounding of the subtraction, <= 3 roundings in the fp32 sum of squares)
-      // with a safety factor 1.5 on every term
-      const double a = 1.5 * u, b = 1.5 * u * C, g = 4.5 * u, delta = 1e-12;
-      const double A = (r * (1.0 + delta) + b) / (1.0 - a);
-      tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15));
-      const double B = (r * (1.0 - delta) - b) / (1.0 + a);
-      trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 1e-15)) : -INFINITY;
-      // Levels 20-21: fp32 quantisation can place a particle up to 0.19 grid
-      // quanta outside its key-space cell, so there (and only there) a cell
-      // containing the target could pass s/d < theta for theta < 1/sqrt(3).
-      // The fast walk skips the containment test (walk.cu); never accepting
-      // these cells in the fp32 filter routes every such decision to the exact
-      // re-walk, which tests containment.
-      if (level >= 20) tacc = INFINITY;
-    }
-    Rec r;
-    r.cm = make_float4(fx, fy, fz, __double2float_rn(M));
-    r.aux = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), skip,
-                       (uint32_t)level | (level == BH_MAXLEVEL ? META_BUCKET : 0u));
-    rec[c] = r;
   }
+  for (uint32_t j = lo + BH_MOM_PREFETCH; j < hi; j++) {
+    const double4 r = lvl_mom[off1 + j];
+    M = __dadd_rn(M, r.x);
+    X = __dadd_rn(X, r.y);
+    Y = __dadd_rn(Y, r.z);
+    Z = __dadd_rn(Z, r.w);
+  }
+  lvl_mom[off + t] = make_double4(M, X, Y, Z);
+  lvl_skip[off + t] = skip;
+  const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
+  const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
+  if (QUAD) {
+    // the quadrupole about (cx, cy, cz): the children in digit order, each its
+    // own Q plus its mass at its com's offset (parallel-axis rule)
+    double Q[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (uint32_t j = lo; j < hi; j++) {
+      const uint32_t ec = item_rec[off1 + j];
+      if (ec & ITEM_LEAF) {
+        const float4 pp = rec[ec & ~ITEM_LEAF].cm;
+        add_point_quad(Q, (double)pp.w, __dsub_rn((double)pp.x, cx), __dsub_rn((double)pp.y, cy),
+                       __dsub_rn((double)pp.z, cz));
+      } else {
+        const double *qc = lvl_q + 6 * (size_t)(off1 + j);
+#pragma unroll
+        for (int k = 0; k < 6; k++) Q[k] = __dadd_rn(Q[k], qc[k]);
+        const double4 mc = lvl_mom[off1 + j];
+        add_point_quad(Q, mc.x, __dsub_rn(__ddiv_rn(mc.y, mc.x), cx), __dsub_rn(__ddiv_rn(mc.z, mc.x), cy),
+                       __dsub_rn(__ddiv_rn(mc.w, mc.x), cz));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      qmom[6 * (size_t)c + k] = Q[k];
+      lvl_q[6 * (size_t)(off + t) + k] = Q[k];
+    }
+    // the walk's copy is -Q in fp32 (walk.cu: the minus sign of the field's
+    // first term rides on Q, exactly)
+    qrec[2 * (size_t)c] = make_float4(-__double2float_rn(Q[0]), -__double2float_rn(Q[1]),
+                                      -__double2float_rn(Q[2]), -__double2float_rn(Q[3]));
+    qrec[2 * (size_t)c + 1] = make_float4(-__double2float_rn(Q[4]), -__double2float_rn(Q[5]), 0.f, 0.f);
+  }
+  float tacc, trej;
+  if (!(theta > 0.0)) {
+    tacc = INFINITY;
+    trej = INFINITY;
+  } else {
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    const double s = ldexp(Ld, -level);
+    const double r = s / theta;
+    const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
+    // first-order bounds (u: com rounding |c32 - c64| <= u(1+u)|c32|, one
+    // rounding of the subtraction, <= 3 roundings in the fp32 sum of squares)
+    // with a safety factor 1.5 on every term
+    const double a = 1.5 * u, b = 1.5 * u * C, g = 4.5 * u, delta = 1e-12;
+    const double A = (r * (1.0 + delta) + b) / (1.0 - a);
+    tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15));
+    const double B = (r * (1.0 - delta) - b) / (1.0 + a);
+    trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 1e-15)) : -INFINITY;
+    // Levels 20-21: fp32 quantisation can place a particle up to 0.19 grid
+    // quanta outside its key-space cell, so there (and only there) a cell
+    // containing the target could pass s/d < theta for theta < 1/sqrt(3).
+    // The fast walk skips the containment test (walk.cu); never accepting
+    // these cells in the fp32 filter routes every such decision to the exact
+    // re-walk, which tests containment.
+    if (level >= 20) tacc = INFINITY;
+  }
+  Rec r;
+  r.cm = make_float4(fx, fy, fz, __double2float_rn(M));
+  r.aux = make_uint4(__float_as_uint(tacc), __float_as_uint(trej), skip,
+                     (uint32_t)level | (level == BH_MAXLEVEL ? META_BUCKET : 0u));
+  rec[c] = r;
 }
 
 template <bool QUAD>
