@@ -104,9 +104,11 @@ size_t bh_workspace_bytes(const bh_params *p);
 bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const float *pos,
                     const float *vel, int where);
 
-/* Replace the state (user order; vel may be NULL = zero).  Keeps the storage
- * order of bh_create and resets the step counter (the next bh_step applies the
- * half kick, reading L8).  Asynchronous for BH_DEVICE inputs. */
+/* Replace the state (user order; vel may be NULL = zero; mass may be NULL =
+ * keep the current masses, so a caller that only moves particles sends 24 B per
+ * particle).  Keeps the storage order of bh_create and resets the step counter
+ * (the next bh_step applies the half kick, reading L8).  Asynchronous for
+ * BH_DEVICE inputs. */
 bh_status bh_set_state(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int where);
 
 /* K0-K5: root cube, Morton keys, radix sort, octree, mass / centre of mass on

@@ -208,15 +208,18 @@ class BarnesHut:
 
     # ------------------------------------------------------------------ ABI
     def set_state(self, mass, pos, vel=None):
+        """Replace positions / velocities (user order); `mass` None keeps the
+        current masses, `vel` None means zero velocities."""
         torch = self.torch
         if isinstance(pos, torch.Tensor) and pos.is_cuda:
-            self._keep = (mass.contiguous().float(), pos.contiguous().float(),
+            self._keep = (None if mass is None else mass.contiguous().float(), pos.contiguous().float(),
                           None if vel is None else vel.contiguous().float())
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
             self._chk(self.L.bh_set_state(self.h, *map(_ptr, self._keep), BH_DEVICE))
         else:
             n = self.n
-            m_, p_ = _host_f32(mass, (n,)), _host_f32(pos, (n, 3))
+            m_ = None if mass is None else _host_f32(mass, (n,))
+            p_ = _host_f32(pos, (n, 3))
             v_ = None if vel is None else _host_f32(vel, (n, 3))
             self._chk(self.L.bh_set_state(self.h, _ptr(m_), _ptr(p_), _ptr(v_), BH_HOST))
             self._chk(self.L.bh_sync(self.h))

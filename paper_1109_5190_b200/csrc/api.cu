@@ -207,7 +207,8 @@ __global__ void k_load_state(float4 *__restrict__ pos4, float4 *__restrict__ vel
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n) return;
   uint32_t u = uid[s];
-  pos4[s] = make_float4(pos[3 * (size_t)u], pos[3 * (size_t)u + 1], pos[3 * (size_t)u + 2], mass[u]);
+  pos4[s] = make_float4(pos[3 * (size_t)u], pos[3 * (size_t)u + 1], pos[3 * (size_t)u + 2],
+                        mass ? mass[u] : pos4[s].w);  // no masses: keep the current ones
   if (s >= lo && s < hi)
     vel4[s - lo] = vel ? make_float4(vel[3 * (size_t)u], vel[3 * (size_t)u + 1], vel[3 * (size_t)u + 2], 0.f)
                        : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -495,9 +496,9 @@ static bh_status stage_inputs(bh_ctx *ctx, const float *mass, const float *pos, 
   float *sm = (float *)ctx->W.targets;
   float *sv = (float *)ctx->W.rec;
   CK(cudaMemcpyAsync(sp, pos, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(sm, mass, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (mass) CK(cudaMemcpyAsync(sm, mass, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (vel) CK(cudaMemcpyAsync(sv, vel, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->stream));
-  *dm = sm; *dp = sp; *dv = vel ? sv : nullptr;
+  *dm = mass ? sm : nullptr; *dp = sp; *dv = vel ? sv : nullptr;
   return BH_OK;
 }
 
@@ -633,7 +634,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
 }
 
 bh_status bh_set_state(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int where) {
-  if (!ctx || !mass || !pos || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  if (!ctx || !pos || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
   bh_status st = set_dev(ctx);
   if (st) return st;
   const int64_t n = ctx->p.n;

@@ -300,6 +300,14 @@ def test_device_pointer_paths(BH):
     bh.step(1)
     bh.get_state(po, vo)
     assert np.array_equal(po.cpu().numpy(), hp)
+    # mass None keeps the masses (device and host inputs)
+    bh.set_state(None, dp, dv)
+    bh.step(1)
+    bh.get_state(po, vo)
+    assert np.array_equal(po.cpu().numpy(), hp)
+    host.set_state(None, p, v)
+    host.step(1)
+    assert np.array_equal(host.get_state()[0], hp)
 
 
 @pytest.mark.parametrize("near", ["0", "1"])
