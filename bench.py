@@ -312,25 +312,24 @@ def ours_arm(args):
         op = torch.empty((cfg.n, 3), dtype=torch.float32).pin_memory().numpy()
         ov = torch.empty((cfg.n, 3), dtype=torch.float32).pin_memory().numpy()
         bh.set_state(hm, hp, hv)
-        bh.step(1)
-        bh.get_state()  # warm the path
+        bh.advance(None, hp, hv, 1, op, ov)  # warm the path
         e_steps = max(1, min(args.steps, 5))
         barrier()
         torch.cuda.synchronize()
         s0 = bh.get_stats()["interactions_cum"]
         t0 = time.perf_counter()
         for _ in range(e_steps):
-            bh.set_state(None, hp, hv)  # masses do not change: kept on the device
-            bh.step(1)
-            bh.L.bh_get_state(bh.h, bhmod._ptr(op), bhmod._ptr(ov), bhmod.BH_HOST)
+            # one bh_advance per step: positions + velocities in (masses do not
+            # change and stay on the device), one step, positions + velocities out
+            bh.advance(None, hp, hv, 1, op, ov)
         torch.cuda.synchronize()
         t_e = allreduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None)
         e_inter = allreduce(float(bh.get_stats()["interactions_cum"] - s0), dist.ReduceOp.SUM if world > 1 else None)
         e2e = {"value": e_inter / t_e, "unit": UNIT, "h2d_bytes_per_step": int(cfg.n * (12 + 12)),
                "d2h_bytes_per_step": int(cfg.n * (12 + 12)), "steps": e_steps,
                "ms_per_step": t_e / e_steps * 1e3,
-               "path": "bh_set_state(pinned host positions + velocities, masses kept) + bh_step(1) + "
-                       "bh_get_state(pinned host) per step"}
+               "path": "bh_advance(pinned host positions + velocities in, masses kept; 1 step; positions + "
+                       "velocities out) per step"}
 
     # ownership balance for P = 2/4/8 from this GPU's per-particle costs (the
     # last walk's interaction counts, storage order): the even Morton-range split

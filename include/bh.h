@@ -131,6 +131,16 @@ bh_status bh_compute_forces(bh_ctx *ctx, float *acc, int where);
  * only this rank's slice advances).  Asynchronous. */
 bh_status bh_step(bh_ctx *ctx, int nsteps);
 
+/* bh_set_state(mass, pos, vel, where) + bh_step(nsteps) + bh_get_state(pos_out,
+ * vel_out, where) in one call, for callers that keep the state on the host:
+ * the velocities (read only by the first walk's leapfrog) are uploaded on a
+ * second stream while the first tree is built, after the positions.  mass NULL
+ * keeps the masses, vel NULL means zero velocities, pos_out / vel_out NULL skip
+ * that output.  Synchronous: every buffer is borrowed only for the call.
+ * Results are identical to the three calls. */
+bh_status bh_advance(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int nsteps, float *pos_out,
+                     float *vel_out, int where);
+
 /* Wait for all enqueued work; report device-side errors. */
 bh_status bh_sync(bh_ctx *ctx);
 

@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH):
             "bh_build_tree": (i32, [vp]),
             "bh_compute_forces": (i32, [vp, vp, i32]),
             "bh_step": (i32, [vp, i32]),
+            "bh_advance": (i32, [vp, vp, vp, vp, i32, vp, vp, i32]),
             "bh_sync": (i32, [vp]),
             "bh_destroy": (i32, [vp]),
             "bh_get_state": (i32, [vp, vp, vp, i32]),
@@ -242,6 +243,34 @@ class BarnesHut:
 
     def step(self, nsteps=1):
         self._chk(self.L.bh_step(self.h, int(nsteps)))
+
+    def advance(self, mass, pos, vel, nsteps=1, pos_out=None, vel_out=None):
+        """set_state(mass, pos, vel) + step(nsteps) + get_state in one call
+        (bh_advance: the velocity upload overlaps the first tree build).  Host
+        arrays in -> host arrays out (allocated if not given); CUDA tensors in ->
+        CUDA tensors out (pos_out / vel_out required, or None to skip).
+        `mass` None keeps the masses, `vel` None means zero velocities."""
+        torch = self.torch
+        n = self.n
+        if isinstance(pos, torch.Tensor) and pos.is_cuda:
+            keep = (None if mass is None else mass.contiguous().float(), pos.contiguous().float(),
+                    None if vel is None else vel.contiguous().float())
+            cur = torch.cuda.current_stream(self.device)
+            self.stream.wait_stream(cur)
+            self._chk(self.L.bh_advance(self.h, _ptr(keep[0]), _ptr(keep[1]), _ptr(keep[2]), int(nsteps),
+                                        _ptr(pos_out), _ptr(vel_out), BH_DEVICE))
+            cur.wait_stream(self.stream)
+            return pos_out, vel_out
+        m_ = None if mass is None else _host_f32(mass, (n,))
+        p_ = _host_f32(pos, (n, 3))
+        v_ = None if vel is None else _host_f32(vel, (n, 3))
+        if pos_out is None:
+            pos_out = np.zeros((n, 3), np.float32)
+        if vel_out is None:
+            vel_out = np.zeros((n, 3), np.float32)
+        self._chk(self.L.bh_advance(self.h, _ptr(m_), _ptr(p_), _ptr(v_), int(nsteps), _ptr(pos_out), _ptr(vel_out),
+                                    BH_HOST))
+        return pos_out, vel_out
 
     def sync(self):
         self._chk(self.L.bh_sync(self.h))

@@ -45,6 +45,11 @@ struct bh_ctx {
   int near_sort;        // 1: try the near-sorted path each build (nearsort.cu)
   DevStatus *hstatus;  // pinned
   cudaEvent_t status_ev;
+  // bh_advance: the velocity upload runs on io_stream beside the first build
+  cudaStream_t io_stream;
+  cudaEvent_t io_ev_pos, io_ev_vel;
+  bool vel_pending;      // vel4 still to be loaded from vel_src before the next walk
+  const float *vel_src;  // device copy of the user-order velocities (null: zero)
   bool status_pending;
   char err[512];
   // profiling
@@ -119,7 +124,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
       (size_t)L.cap_rec * 32,                  // 16 rec (cm + aux)
       (size_t)L.cap_resume * sizeof(ResumeState),  // 17 walk resume states
       (size_t)L.cap_rec * 4,                   // 18 rec_item: level-item index of each record
-      0,                                       // 19 (unused)
+      (size_t)n * 12,                          // 19 bh_advance: user-order velocities in flight
       (size_t)L.cap_rec * 4,                   // 20 item_rec (level-ordered items)
       (size_t)n * 4,                           // 21 redo list
       (size_t)n * 4,                           // 22 walk cost per particle (its group's trips)
@@ -164,6 +169,7 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.resume = (ResumeState *)(b + L.off[17]);
   W.cap_resume = L.cap_resume;
   W.rec_item = (uint32_t *)(b + L.off[18]);
+  W.vstage = (float *)(b + L.off[19]);
   W.item_rec = (uint32_t *)(b + L.off[20]);
   W.item_clo = (uint32_t *)(b + L.off[25]);
   W.lvl_skip = (uint32_t *)(b + L.off[26]);
@@ -212,6 +218,24 @@ __global__ void k_load_state(float4 *__restrict__ pos4, float4 *__restrict__ vel
   if (s >= lo && s < hi)
     vel4[s - lo] = vel ? make_float4(vel[3 * (size_t)u], vel[3 * (size_t)u + 1], vel[3 * (size_t)u + 2], 0.f)
                        : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// bh_advance: positions (+ masses, or the current ones) and, later, the own
+// slice's velocities, user order -> storage order
+__global__ void k_load_pos(float4 *__restrict__ pos4, const uint32_t *__restrict__ uid, const float *__restrict__ pos,
+                           const float *__restrict__ mass, int64_t n) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  uint32_t u = uid[s];
+  pos4[s] = make_float4(pos[3 * (size_t)u], pos[3 * (size_t)u + 1], pos[3 * (size_t)u + 2], mass ? mass[u] : pos4[s].w);
+}
+__global__ void k_load_vel(float4 *__restrict__ vel4, const uint32_t *__restrict__ uid, const float *__restrict__ vel,
+                           int64_t lo, int64_t hi) {
+  int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  uint32_t u = uid[s];
+  vel4[s - lo] = vel ? make_float4(vel[3 * (size_t)u], vel[3 * (size_t)u + 1], vel[3 * (size_t)u + 2], 0.f)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // user-order outputs from storage slots [lo, hi): out[uid[s]] = src(s)
@@ -574,6 +598,10 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->num_sms = 148;
   ctx->sort_buf = 0;
   ctx->status_pending = false;
+  ctx->io_stream = nullptr;
+  ctx->io_ev_pos = ctx->io_ev_vel = nullptr;
+  ctx->vel_pending = false;
+  ctx->vel_src = nullptr;
   bh_status st = BH_OK;
   do {
     if (cudaSetDevice(p->device) != cudaSuccess) { st = fail(ctx, BH_ERR_CUDA, "cudaSetDevice(%d) failed", p->device); break; }
@@ -643,6 +671,7 @@ bh_status bh_set_state(bh_ctx *ctx, const float *mass, const float *pos, const f
   if (st) return st;
   k_load_state<<<blocks_for(n), 256, 0, ctx->stream>>>(ctx->W.pos4, ctx->W.vel4, ctx->W.uid, dp, dm, dv, n,
                                                         ctx->own_lo, ctx->own_hi);
+  ctx->vel_pending = false;  // (a pending bh_advance upload is superseded)
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(&ctx->W.status->err, 0, sizeof(uint32_t), ctx->stream));
   ctx->steps = 0;
@@ -692,8 +721,22 @@ bh_status bh_compute_forces(bh_ctx *ctx, float *acc, int where) {
 }
 
 // one time step's launches (K0-K8) on ctx->stream
+// bh_advance's velocities: wait for their upload and load the own slice
+static bh_status flush_vel(bh_ctx *ctx) {
+  if (!ctx->vel_pending) return BH_OK;
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->io_ev_vel, 0));
+  const int64_t own_n = ctx->own_hi - ctx->own_lo;
+  k_load_vel<<<blocks_for(own_n), 256, 0, ctx->stream>>>(ctx->W.vel4, ctx->W.uid, ctx->vel_src, ctx->own_lo,
+                                                          ctx->own_hi);
+  CK(cudaGetLastError());
+  ctx->vel_pending = false;
+  return BH_OK;
+}
+
 static bh_status enqueue_step(bh_ctx *ctx, float kick) {
   bh_status st = build_tree(ctx);
+  if (st) return st;
+  st = flush_vel(ctx);  // bh_advance: the velocity upload ran beside the build
   if (st) return st;
   st = walk(ctx, 1, kick, nullptr, false);
   if (st) return st;
@@ -746,8 +789,9 @@ bh_status bh_step(bh_ctx *ctx, int nsteps) {
     st = status_from_device(ctx);
     if (st) return st;
   }
-  const bool graphs = ctx->use_graphs && !ctx->prof && !(ctx->p.world > 1 && ctx->p.nccl_comm);
   for (int k = 0; k < nsteps; k++) {
+    // (a captured step must not contain bh_advance's one-off velocity load)
+    const bool graphs = ctx->use_graphs && !ctx->prof && !(ctx->p.world > 1 && ctx->p.nccl_comm) && !ctx->vel_pending;
     if (ctx->prof) ctx->prof_calls++;
     const int which = ctx->steps == 0 ? 0 : 1;
     const float kick = (float)(which == 0 ? 0.5 * ctx->p.dt : ctx->p.dt);
@@ -782,6 +826,10 @@ bh_status bh_destroy(bh_ctx *ctx) {
   for (auto e : ctx->free_events) cudaEventDestroy(e);
   drop_graphs(ctx);
   if (ctx->status_ev) cudaEventDestroy(ctx->status_ev);
+  if (ctx->io_stream) cudaStreamSynchronize(ctx->io_stream);
+  if (ctx->io_ev_pos) cudaEventDestroy(ctx->io_ev_pos);
+  if (ctx->io_ev_vel) cudaEventDestroy(ctx->io_ev_vel);
+  if (ctx->io_stream) cudaStreamDestroy(ctx->io_stream);
   if (ctx->hstatus) cudaFreeHost(ctx->hstatus);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -791,6 +839,8 @@ bh_status bh_destroy(bh_ctx *ctx) {
 bh_status bh_get_state(bh_ctx *ctx, float *pos, float *vel, int where) {
   if (!ctx || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
   bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = flush_vel(ctx);
   if (st) return st;
   const int64_t n = ctx->p.n, lo = ctx->own_lo, hi = ctx->own_hi, own_n = hi - lo;
   cudaStream_t s = ctx->stream;
@@ -822,6 +872,64 @@ bh_status bh_get_state(bh_ctx *ctx, float *pos, float *vel, int where) {
       }
     }
   }
+  return do_sync(ctx);
+}
+
+// set_state + step(nsteps) + get_state in one call: the velocities (needed
+// only by the first walk's leapfrog) are uploaded on a second stream while the
+// first tree is built, after the positions' upload (both share the link).
+bh_status bh_advance(bh_ctx *ctx, const float *mass, const float *pos, const float *vel, int nsteps, float *pos_out,
+                     float *vel_out, int where) {
+  if (!ctx || !pos || nsteps < 0 || (where != BH_HOST && where != BH_DEVICE))
+    return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  if (!ctx->io_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->io_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->io_ev_pos, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->io_ev_vel, cudaEventDisableTiming));
+  }
+  const int64_t n = ctx->p.n;
+  cudaStream_t s = ctx->stream;
+  const float *dp = pos, *dm = mass;
+  if (where == BH_HOST) {
+    CK(cudaMemcpyAsync(ctx->W.accu, pos, (size_t)n * 12, cudaMemcpyHostToDevice, s));
+    if (mass) CK(cudaMemcpyAsync(ctx->W.targets, mass, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    dp = ctx->W.accu;
+    dm = mass ? (const float *)ctx->W.targets : nullptr;
+  }
+  // the velocity upload starts once the positions are in (and after every
+  // earlier use of its staging buffer: the event follows all prior work)
+  CK(cudaEventRecord(ctx->io_ev_pos, s));
+  if (vel && where == BH_HOST) {
+    CK(cudaStreamWaitEvent(ctx->io_stream, ctx->io_ev_pos, 0));
+    CK(cudaMemcpyAsync(ctx->W.vstage, vel, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->io_stream));
+    CK(cudaEventRecord(ctx->io_ev_vel, ctx->io_stream));
+    ctx->vel_src = ctx->W.vstage;
+  } else {
+    CK(cudaEventRecord(ctx->io_ev_vel, s));
+    ctx->vel_src = vel;  // device pointer, or null = zero velocities
+  }
+  ctx->vel_pending = true;
+  k_load_pos<<<blocks_for(n), 256, 0, s>>>(ctx->W.pos4, ctx->W.uid, dp, dm, n);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(&ctx->W.status->err, 0, sizeof(uint32_t), s));
+  ctx->steps = 0;
+  ctx->tree_valid = false;
+  if (nsteps == 0) {
+    st = flush_vel(ctx);
+  } else {
+    // the first step directly (its velocity load sits between build and walk), the rest via bh_step
+    if (ctx->prof) ctx->prof_calls++;
+    st = enqueue_step(ctx, (float)(0.5 * ctx->p.dt));
+    if (st) return st;
+    ctx->steps++;
+    st = bh_step(ctx, nsteps - 1);
+  }
+  if (st) return st;
+  // the caller's input buffers are borrowed only for this call
+  if (ctx->io_stream) CK(cudaStreamSynchronize(ctx->io_stream));
+  if (pos_out || vel_out) return bh_get_state(ctx, pos_out, vel_out, where);
   return do_sync(ctx);
 }
 
@@ -983,6 +1091,8 @@ bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel,
                 (long long)own_n, (long long)ctx->lay.n_own_max);
   if (own_n > 0 && !vel) return fail(ctx, BH_ERR_ARG, "velocities of the new own range required");
   bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = flush_vel(ctx);  // (the new slice's velocities replace them below)
   if (st) return st;
   cudaStream_t s = ctx->stream;
   if (own_n > 0) {

@@ -126,6 +126,7 @@ struct Workspace {
   int64_t cap_resume;
   int resume_stack;     // 0: the full resume LIFO; > 0: a smaller one (test hook)
   uint32_t *rec_item;   // per record: its index in the level-ordered item arrays
+  float *vstage;        // bh_advance: n x 3 user-order velocities (host upload target)
   // level-ordered items (tree.cu): per level, the records in Morton order
   uint32_t *blkcnt;     // [23][blocks of 256 particles]: item counts, then offsets
   uint32_t *item_rec;   // record index | ITEM_LEAF

@@ -310,6 +310,44 @@ def test_device_pointer_paths(BH):
     assert np.array_equal(host.get_state()[0], hp)
 
 
+@pytest.mark.parametrize("nsteps", [0, 1, 3])
+def test_advance_matches_three_calls(BH, nsteps):
+    """bh_advance (velocity upload beside the first build) == bh_set_state +
+    bh_step + bh_get_state, bitwise, for host and device buffers, with and
+    without masses / velocities; later steps (CUDA graphs) continue alike."""
+    import torch
+
+    m, p, v = bhgen.generate("cfg2", n=5000)
+    prm = bhgen.params("cfg2")
+    p2 = p + np.float32(1e-3) * v  # a different state to load
+    a = BH(m, p, v, **prm)
+    b = BH(m, p, v, **prm)
+    a.set_state(m, p2, v)
+    a.step(nsteps)
+    ra = a.get_state()
+    rb = b.advance(m, p2, v, nsteps)
+    assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])
+    a.step(2)
+    b.step(2)
+    assert all(np.array_equal(x, y) for x, y in zip(a.get_state(), b.get_state()))
+    # masses kept, zero velocities
+    a.set_state(None, p, None)
+    a.step(nsteps)
+    ra = a.get_state()
+    rb = b.advance(None, p, None, nsteps)
+    assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])
+    # device buffers
+    dm, dp, dv = (torch.from_numpy(x).cuda() for x in (m, p2, v))
+    po, vo = torch.empty_like(dp), torch.empty_like(dv)
+    b.advance(dm, dp, dv, nsteps, po, vo)
+    a.set_state(m, p2, v)
+    a.step(nsteps)
+    ra = a.get_state()
+    assert np.array_equal(ra[0], po.cpu().numpy()) and np.array_equal(ra[1], vo.cpu().numpy())
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("near", ["0", "1"])
 def test_sort_vs_lexsort_many_ties(BH, monkeypatch, near):
     """K2 + tie fix-up == numpy lexsort (library routine) on heavy ties, over
