@@ -238,6 +238,22 @@ __global__ void k_load_vel(float4 *__restrict__ vel4, const uint32_t *__restrict
                      : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// K7 apart (bh_advance's first step): v += a kick, x += v dt, as the walk's
+// fused epilogue does it (acc: own slice, storage order, G applied)
+__global__ void k_kick_drift(float4 *__restrict__ pos4, float4 *__restrict__ vel4, const float *__restrict__ acc,
+                             int64_t lo, int64_t hi, float kick, float dt) {
+  int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  const size_t o = (size_t)(s - lo);
+  float4 v = vel4[o];
+  v.x = fmaf(acc[3 * o + 0], kick, v.x);
+  v.y = fmaf(acc[3 * o + 1], kick, v.y);
+  v.z = fmaf(acc[3 * o + 2], kick, v.z);
+  vel4[o] = v;
+  const float4 x = pos4[s];
+  pos4[s] = make_float4(fmaf(v.x, dt, x.x), fmaf(v.y, dt, x.y), fmaf(v.z, dt, x.z), x.w);
+}
+
 // user-order outputs from storage slots [lo, hi): out[uid[s]] = src(s)
 // own-slice velocities [k][3] (storage order) -> vel4[k]
 __global__ void k_vel3to4(float4 *__restrict__ vel4, const float *__restrict__ v3, int64_t m) {
@@ -736,9 +752,21 @@ static bh_status flush_vel(bh_ctx *ctx) {
 static bh_status enqueue_step(bh_ctx *ctx, float kick) {
   bh_status st = build_tree(ctx);
   if (st) return st;
-  st = flush_vel(ctx);  // bh_advance: the velocity upload ran beside the build
-  if (st) return st;
-  st = walk(ctx, 1, kick, nullptr, false);
+  if (ctx->vel_pending) {
+    // first step of bh_advance: the walk computes forces (own slice, storage
+    // order) while the velocity upload finishes, then K7 runs apart with the
+    // walk epilogue's exact operations (finish() in walk_common.cuh)
+    st = walk(ctx, 0, 0.f, ctx->W.accu, false);
+    if (st) return st;
+    st = flush_vel(ctx);
+    if (st) return st;
+    const int64_t own_n = ctx->own_hi - ctx->own_lo;
+    k_kick_drift<<<blocks_for(own_n), 256, 0, ctx->stream>>>(ctx->W.pos4, ctx->W.vel4, ctx->W.accu, ctx->own_lo,
+                                                              ctx->own_hi, kick, (float)ctx->p.dt);
+    CK(cudaGetLastError());
+  } else {
+    st = walk(ctx, 1, kick, nullptr, false);
+  }
   if (st) return st;
   return exchange(ctx);
 }
