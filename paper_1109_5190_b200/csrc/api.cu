@@ -39,7 +39,7 @@ struct bh_ctx {
   bool walked;
   int walk_stats;
   int use_graphs;
-  cudaGraphExec_t step_graph[2];  // [0]: half kick (first step), [1]: full kick
+  cudaGraphExec_t step_graph[3];  // [0]: half kick (first step), [1]: full kick, [2]: bh_advance's first step
   int num_sms;
   int sort_buf;
   int near_sort;        // 1: try the near-sorted path each build (nearsort.cu)
@@ -610,7 +610,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   // the near-sorted path pays for its ~20 launches from ~2^18 particles on
   // (measured: cfg2, 2^16, 2% slower with it; cfg3, 2^20, 7% faster)
   ctx->near_sort = getenv("BH_NO_NEAR_SORT") ? 0 : (p->n >= ((int64_t)1 << 18) || getenv("BH_NEAR_SORT") ? 1 : 0);
-  ctx->step_graph[0] = ctx->step_graph[1] = nullptr;
+  ctx->step_graph[0] = ctx->step_graph[1] = ctx->step_graph[2] = nullptr;
   ctx->num_sms = 148;
   ctx->sort_buf = 0;
   ctx->status_pending = false;
@@ -740,7 +740,10 @@ bh_status bh_compute_forces(bh_ctx *ctx, float *acc, int where) {
 // bh_advance's velocities: wait for their upload and load the own slice
 static bh_status flush_vel(bh_ctx *ctx) {
   if (!ctx->vel_pending) return BH_OK;
-  CK(cudaStreamWaitEvent(ctx->stream, ctx->io_ev_vel, 0));
+  // (inside graph [2] the event was recorded outside the capture: an external wait node)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(ctx->stream, &cs));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->io_ev_vel, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
   const int64_t own_n = ctx->own_hi - ctx->own_lo;
   k_load_vel<<<blocks_for(own_n), 256, 0, ctx->stream>>>(ctx->W.vel4, ctx->W.uid, ctx->vel_src, ctx->own_lo,
                                                           ctx->own_hi);
@@ -772,7 +775,7 @@ static bh_status enqueue_step(bh_ctx *ctx, float kick) {
 }
 
 static void drop_graphs(bh_ctx *ctx) {
-  for (int i = 0; i < 2; i++)
+  for (int i = 0; i < 3; i++)
     if (ctx->step_graph[i]) {
       cudaGraphExecDestroy(ctx->step_graph[i]);
       ctx->step_graph[i] = nullptr;
@@ -790,9 +793,14 @@ static bh_status step_graph(bh_ctx *ctx, int which, float kick, cudaGraphExec_t 
     return BH_OK;
   }
   cudaGraph_t g = nullptr;
+  // [2] captures the velocity load of bh_advance (a wait on io_ev_vel, recorded
+  // outside the graph, then k_load_vel from vstage) between build and walk
+  const bool pending = ctx->vel_pending;
+  ctx->vel_pending = which == 2;
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   bh_status st = enqueue_step(ctx, kick);
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  ctx->vel_pending = pending;
   if (st) {
     if (g) cudaGraphDestroy(g);
     return st;
@@ -927,17 +935,19 @@ bh_status bh_advance(bh_ctx *ctx, const float *mass, const float *pos, const flo
     dm = mass ? (const float *)ctx->W.targets : nullptr;
   }
   // the velocity upload starts once the positions are in (and after every
-  // earlier use of its staging buffer: the event follows all prior work)
+  // earlier use of its staging buffer: the event follows all prior work); it
+  // always lands in vstage (device inputs are copied, none = zeros), so the
+  // captured first step reads a fixed buffer
   CK(cudaEventRecord(ctx->io_ev_pos, s));
-  if (vel && where == BH_HOST) {
-    CK(cudaStreamWaitEvent(ctx->io_stream, ctx->io_ev_pos, 0));
-    CK(cudaMemcpyAsync(ctx->W.vstage, vel, (size_t)n * 12, cudaMemcpyHostToDevice, ctx->io_stream));
-    CK(cudaEventRecord(ctx->io_ev_vel, ctx->io_stream));
-    ctx->vel_src = ctx->W.vstage;
+  CK(cudaStreamWaitEvent(ctx->io_stream, ctx->io_ev_pos, 0));
+  if (vel) {
+    CK(cudaMemcpyAsync(ctx->W.vstage, vel, (size_t)n * 12,
+                       where == BH_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->io_stream));
   } else {
-    CK(cudaEventRecord(ctx->io_ev_vel, s));
-    ctx->vel_src = vel;  // device pointer, or null = zero velocities
+    CK(cudaMemsetAsync(ctx->W.vstage, 0, (size_t)n * 12, ctx->io_stream));
   }
+  CK(cudaEventRecord(ctx->io_ev_vel, ctx->io_stream));
+  ctx->vel_src = ctx->W.vstage;
   ctx->vel_pending = true;
   k_load_pos<<<blocks_for(n), 256, 0, s>>>(ctx->W.pos4, ctx->W.uid, dp, dm, n);
   CK(cudaGetLastError());
@@ -947,11 +957,23 @@ bh_status bh_advance(bh_ctx *ctx, const float *mass, const float *pos, const flo
   if (nsteps == 0) {
     st = flush_vel(ctx);
   } else {
-    // the first step directly (its velocity load sits between build and walk), the rest via bh_step
+    // the first step (its velocity load sits between build and walk) as its
+    // own captured graph, the rest via bh_step
     if (ctx->prof) ctx->prof_calls++;
-    st = enqueue_step(ctx, (float)(0.5 * ctx->p.dt));
-    if (st) return st;
+    const float kick = (float)(0.5 * ctx->p.dt);
+    if (ctx->use_graphs && !ctx->prof && !(ctx->p.world > 1 && ctx->p.nccl_comm)) {
+      cudaGraphExec_t ge;
+      st = step_graph(ctx, 2, kick, &ge);
+      if (st) return st;
+      CK(cudaGraphLaunch(ge, s));
+      ctx->sort_buf = 0;
+      ctx->vel_pending = false;
+    } else {
+      st = enqueue_step(ctx, kick);
+      if (st) return st;
+    }
     ctx->steps++;
+    ctx->tree_valid = false;
     st = bh_step(ctx, nsteps - 1);
   }
   if (st) return st;

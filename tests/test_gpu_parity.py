@@ -310,12 +310,17 @@ def test_device_pointer_paths(BH):
     assert np.array_equal(host.get_state()[0], hp)
 
 
+@pytest.mark.parametrize("graphs", [True, False])
 @pytest.mark.parametrize("nsteps", [0, 1, 3])
-def test_advance_matches_three_calls(BH, nsteps):
-    """bh_advance (velocity upload beside the first build) == bh_set_state +
-    bh_step + bh_get_state, bitwise, for host and device buffers, with and
-    without masses / velocities; later steps (CUDA graphs) continue alike."""
+def test_advance_matches_three_calls(BH, nsteps, graphs, monkeypatch):
+    """bh_advance (velocity upload beside the first build; its first step a
+    captured graph with an external event wait, or direct launches) ==
+    bh_set_state + bh_step + bh_get_state, bitwise, for host and device
+    buffers, with and without masses / velocities; later steps continue alike."""
     import torch
+
+    if not graphs:
+        monkeypatch.setenv("BH_NO_GRAPHS", "1")
 
     m, p, v = bhgen.generate("cfg2", n=5000)
     prm = bhgen.params("cfg2")
