@@ -28,9 +28,11 @@
  *   - All device memory is carved out of the caller's `workspace`
  *     (bh_workspace_bytes); the library never calls cudaMalloc.  The workspace
  *     must stay allocated until bh_destroy.  Besides it the library owns only a
- *     few hundred bytes of pinned host status memory and CUDA events.
+ *     few hundred bytes of pinned host status memory, CUDA events and (once
+ *     bh_advance is called) a second stream for its velocity upload.
  *   - All device work is enqueued on params.stream (NULL: a library-owned
- *     non-blocking stream).  bh_build_tree, bh_compute_forces with a device
+ *     non-blocking stream); bh_advance's upload stream is joined to it by an
+ *     event and drained before bh_advance returns.  bh_build_tree, bh_compute_forces with a device
  *     output and bh_step are asynchronous; errors found on the device (non-finite
  *     positions, infinite forces, node-capacity overflow) are reported by the
  *     next synchronising call: bh_sync, any getter, a BH_HOST output, or the next
