@@ -353,6 +353,24 @@ def test_advance_matches_three_calls(BH, nsteps, graphs, monkeypatch):
     b.close()
 
 
+def test_advance_multirank_matches_three_calls(BH):
+    """bh_advance on a rank of a multi-rank ctx (own velocity slice, host
+    scatter of the velocities) == bh_set_state + bh_step + bh_get_state."""
+    m, p, v = bhgen.generate("cfg2", n=6000)
+    prm = bhgen.params("cfg2")
+    p2 = p + np.float32(1e-3) * v
+    for r in range(2):
+        a = BH(m, p, v, rank=r, world=2, **prm)
+        b = BH(m, p, v, rank=r, world=2, **prm)
+        b.set_state(m, p2, v)
+        b.step(1)
+        rb = b.get_state()
+        ra = a.advance(None, p2, v, 1)
+        assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])
+        a.close()
+        b.close()
+
+
 @pytest.mark.parametrize("near", ["0", "1"])
 def test_sort_vs_lexsort_many_ties(BH, monkeypatch, near):
     """K2 + tie fix-up == numpy lexsort (library routine) on heavy ties, over
