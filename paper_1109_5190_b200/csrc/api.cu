@@ -43,6 +43,7 @@ struct bh_ctx {
   int num_sms;
   int sort_buf;
   int near_sort;        // 1: try the near-sorted path each build (nearsort.cu)
+  int cont_fold;        // containment folded into T_acc (com.cu): the walk skips its per-visit test
   DevStatus *hstatus;  // pinned
   cudaEvent_t status_ev;
   // bh_advance: the velocity upload runs on io_stream beside the first build
@@ -104,7 +105,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
   L.blocks = (n + 1 + 255) / 256;  // tree.cu's particle blocks
-  size_t sz[30] = {
+  size_t sz[31] = {
       sizeof(DevStatus),                       // 0 status
       (size_t)n * 16,                          // 1 pos4
       (size_t)L.n_own_max * 16,                // 2 vel4
@@ -135,9 +136,10 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
       (size_t)L.cap_rec * 32,                  // 27 lvl_mom
       multipole == 2 ? (size_t)L.cap_rec * 48 : 0,  // 28 lvl_q
       (size_t)BH_NLEVELS * (L.blocks + (L.blocks + 1023) / 1024) * 4,  // 29 blkcnt + segment sums (tree.cu)
+      (size_t)L.cap_rec * 16,                  // 30 lvl_cm: fp32 com + bounding radius of each item
   };
   size_t off = 0;
-  for (int i = 0; i < 30; i++) {
+  for (int i = 0; i < 31; i++) {
     L.off[i] = off;
     off += align_up(sz[i]);
   }
@@ -176,6 +178,7 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.lvl_mom = (double4 *)(b + L.off[27]);
   W.lvl_q = L.off[28] != L.off[29] ? (double *)(b + L.off[28]) : nullptr;
   W.blkcnt = (uint32_t *)(b + L.off[29]);
+  W.lvl_cm = (float4 *)(b + L.off[30]);
   W.redo = (uint32_t *)(b + L.off[21]);
   W.gcost = (uint32_t *)(b + L.off[22]);
   W.qmom = L.off[23] != L.off[24] ? (double *)(b + L.off[23]) : nullptr;
@@ -440,11 +443,11 @@ static bh_status build_tree(bh_ctx *ctx) {
   prof_end(ctx, &pp, (ctx->near_sort ? 22 : 0) + 2 + SORT_PASSES + 1);
   ctx->sort_buf = buf;
   prof_begin(ctx, &pp, 2);
-  CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, s));  // (zeroes the particles' quadrupoles)
+  CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, ctx->cont_fold, s));  // (zeroes the particles' quadrupoles)
   prof_end(ctx, &pp, 8);
   prof_begin(ctx, &pp, 3);
   int launches = 0;
-  CK(launch_moments(ctx->W, n, ctx->p.theta, s, &launches));
+  CK(launch_moments(ctx->W, n, ctx->p.theta, ctx->cont_fold, s, &launches));
   prof_end(ctx, &pp, launches);
   ctx->tree_valid = true;
   return BH_OK;
@@ -471,7 +474,7 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   // containment test elision (see walk.cu): a cell holding the target has
   // s/d >= 1/sqrt(3) (d <= sqrt(3) s), so it never passes s/d < theta for
   // theta < 0.5773; kept with a margin, and only when eps > 0
-  a.need_cont = !(ctx->p.theta < 0.57 && ctx->p.eps > 0.0);
+  a.need_cont = !(ctx->p.theta < 0.57 && ctx->p.eps > 0.0) && !ctx->cont_fold;
   a.mode = mode;
   a.eps2 = (float)(ctx->p.eps * ctx->p.eps);
   a.G = (float)ctx->p.G;
@@ -609,6 +612,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->use_graphs = getenv("BH_NO_GRAPHS") ? 0 : 1;
   // the near-sorted path pays for its ~20 launches from ~2^18 particles on
   // (measured: cfg2, 2^16, 2% slower with it; cfg3, 2^20, 7% faster)
+  ctx->cont_fold = (p->theta >= 0.57 && p->eps > 0.0 && !getenv("BH_NO_CONT_FOLD")) ? 1 : 0;
   ctx->near_sort = getenv("BH_NO_NEAR_SORT") ? 0 : (p->n >= ((int64_t)1 << 18) || getenv("BH_NEAR_SORT") ? 1 : 0);
   ctx->step_graph[0] = ctx->step_graph[1] = ctx->step_graph[2] = nullptr;
   ctx->num_sms = 148;

@@ -134,6 +134,7 @@ struct Workspace {
   uint32_t *lvl_skip;   // skip() of the item's record
   double4 *lvl_mom;     // fp64 (M, MX, MY, MZ) of the item
   double *lvl_q;        // multipole = 2: fp64 quadrupole of the item (6 per item; null otherwise)
+  float4 *lvl_cm;       // (com32.xyz, bounding radius) of each item (containment folded into T_acc)
   DevStatus *status;
 };
 
@@ -167,8 +168,9 @@ cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *fina
 cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s);
 cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s);
 cudaError_t launch_tie_fixup(const Workspace &W, int64_t n, int buf, cudaStream_t s);
-cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, cudaStream_t s);
-cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, cudaStream_t s, int *launches);
+cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, int cont_fold, cudaStream_t s);
+cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont_fold, cudaStream_t s,
+                           int *launches);
 cudaError_t launch_scan_u32(uint32_t *data, int64_t count, uint32_t *tmp, cudaStream_t s);
 cudaError_t launch_own_targets(const Workspace &W, int64_t n, int buf, uint32_t own_lo, uint32_t own_hi,
                                cudaStream_t s);

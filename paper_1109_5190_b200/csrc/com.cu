@@ -68,6 +68,21 @@ __device__ __forceinline__ void add_point_quad(double Q[6], double m, double y0,
   Q[5] = __dadd_rn(Q[5], __dmul_rn(m, __dmul_rn(__dmul_rn(3.0, y1), y2)));
 }
 
+// Containment folded into the fp32 filter (theta >= 0.57 with eps > 0, so the
+// fast walk needs no per-visit containment test).  Every item carries a
+// bounding radius R about its fp32 com: R(particle) = 0, R(node) >= max over
+// children of |com - com32_child| + R_child (+ the child's com rounding), so
+// every particle of the node lies within R of its com, and a target inside the
+// node (one of its particles) is at distance <= R.  T_acc is raised to the
+// bound of R (the T_acc error model with r -> R): a node that may contain the
+// target is then never accepted for sure, and the band between T_rej and that
+// bound goes to the exact re-walk, which tests containment (reading L5).  For
+// most nodes R < s/theta already and nothing changes.
+struct ContFold {
+  float4 *lvl_cm;
+  int on;
+};
+
 // one internal node of level `level` at item t (record c, children [lo, hi) of the next level)
 template <bool QUAD>
 __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, uint32_t lo, uint32_t hi, uint32_t off,
@@ -75,7 +90,8 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
                                              const uint32_t *__restrict__ item_rec, uint32_t *__restrict__ lvl_skip,
                                              double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
                                              double *__restrict__ lvl_q,
-                                             double *__restrict__ qmom, float4 *__restrict__ qrec) {
+                                             double *__restrict__ qmom, float4 *__restrict__ qrec,
+                                             const ContFold cf, const DevStatus *__restrict__ st) {
   const uint32_t skip = lvl_skip[off1 + hi - 1];  // the last child's
   // the children in digit order (reading L14): a particle contributes
   // (m, m x), an internal node its (M, MX); the first BH_MOM_PREFETCH are
@@ -105,6 +121,20 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
   lvl_skip[off + t] = skip;
   const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
   const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
+  double Rn = 0.0;
+  if (cf.on) {
+    // bounding radius: the children's fp32 coms and radii (their rounding, u |c|
+    // per axis, added)
+    for (uint32_t j = lo; j < hi; j++) {
+      const float4 q4 = cf.lvl_cm[off1 + j];
+      const double ex = cx - (double)q4.x, ey = cy - (double)q4.y, ez = cz - (double)q4.z;
+      const double r = sqrt(ex * ex + ey * ey + ez * ez) + (double)q4.w +
+                       6.0e-8 * (fabs((double)q4.x) + fabs((double)q4.y) + fabs((double)q4.z));
+      Rn = fmax(Rn, r);
+    }
+    Rn *= 1.0 + 1e-12;
+    cf.lvl_cm[off + t] = make_float4(fx, fy, fz, round_up_f(Rn));
+  }
   if (QUAD) {
     // the quadrupole about (cx, cy, cz): the children in digit order, each its
     // own Q plus its mass at its com's offset (parallel-axis rule)
@@ -159,6 +189,13 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     // these cells in the fp32 filter routes every such decision to the exact
     // re-walk, which tests containment.
     if (level >= 20) tacc = INFINITY;
+    if (cf.on && level < 20) {
+      const double u = 5.9604644775390625e-08;
+      const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
+      const double a = 1.5 * u, b = 1.5 * u * C, g = 4.5 * u;
+      const double A = (Rn * (1.0 + 1e-12) + b) / (1.0 - a);
+      tacc = fmaxf(tacc, round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15)));
+    }
   }
   Rec r;
   r.cm = make_float4(fx, fy, fz, __double2float_rn(M));
@@ -175,7 +212,7 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
                                                        double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
                                                        double theta,
                                                        double *__restrict__ lvl_q, double *__restrict__ qmom,
-                                                       float4 *__restrict__ qrec) {
+                                                       float4 *__restrict__ qrec, const ContFold cf) {
   if (st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t cnt = st->lvl_count[level];
   const uint32_t off = st->lvl_offset[level];
@@ -207,12 +244,16 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
     hi = hin;
     if (ecur & ITEM_LEAF) continue;  // a particle: K4 wrote its record and moments
     moments_node<QUAD>(level, t, ecur, locur, hicur, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec,
-                       lvl_q, qmom, qrec);
+                       lvl_q, qmom, qrec, cf, st);
   }
 }
 
 
-cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, cudaStream_t s, int *launches) {
+cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont_fold, cudaStream_t s,
+                           int *launches) {
+  ContFold cf;
+  cf.lvl_cm = W.lvl_cm;
+  cf.on = cont_fold;
   if (n < 2) return cudaSuccess;
   // grid: enough blocks for the widest level (at most n items), capped at 8
   // waves of 148 SMs
@@ -223,10 +264,10 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, cudaStre
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
     if (W.qmom)
       k_moments_level<true><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom, W.rec,
-                                                 theta, W.lvl_q, W.qmom, W.qrec);
+                                                 theta, W.lvl_q, W.qmom, W.qrec, cf);
     else
       k_moments_level<false><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom,
-                                                  W.rec, theta, W.lvl_q, W.qmom, W.qrec);
+                                                  W.rec, theta, W.lvl_q, W.qmom, W.qrec, cf);
     if (launches) (*launches)++;
   }
   return cudaGetLastError();

@@ -242,6 +242,30 @@ def test_walk_group_invariance(BH, cfg, group):
     assert np.array_equal(a.get_interactions()[0], b.get_interactions()[0])
 
 
+@pytest.mark.parametrize("cfg,group", [("cfg3", 68), ("cfg3", 67), ("cfg3", 1), ("cfg3", 83), ("cfg5", 68)])
+def test_containment_fold_vs_test(BH, cfg, group, monkeypatch):
+    """theta >= 0.57: containment folded into T_acc through the nodes' bounding
+    radii (no per-visit test) == the walk that tests containment per visit:
+    identical interaction counts; forces bitwise equal when no extra target
+    fell back to the exact re-walk (else within fp32 rounding)."""
+    m, p, v = bhgen.generate(cfg, n=30000)
+    prm = bhgen.params(cfg)
+    a = BH(m, p, v, walk_group=group, **prm)  # fold (default for theta >= 0.57, eps > 0)
+    a.build_tree()
+    fa = a.compute_forces()
+    ra = a.get_stats()["redo_targets"]
+    monkeypatch.setenv("BH_NO_CONT_FOLD", "1")
+    b = BH(m, p, v, walk_group=group, **prm)
+    b.build_tree()
+    fb = b.compute_forces()
+    rb = b.get_stats()["redo_targets"]
+    assert np.array_equal(a.get_interactions()[0], b.get_interactions()[0])
+    if ra == rb:
+        assert np.array_equal(fa, fb)
+    else:
+        assert np.allclose(fa, fb, rtol=1e-5, atol=0)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_rank_emulation_bitwise(BH, world):
     """Multi-GPU path emulated on one GPU (no NCCL): each rank's walk over its
