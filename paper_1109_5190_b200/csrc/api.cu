@@ -136,7 +136,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
       (size_t)L.cap_rec * 32,                  // 27 lvl_mom
       multipole == 2 ? (size_t)L.cap_rec * 48 : 0,  // 28 lvl_q
       (size_t)BH_NLEVELS * (L.blocks + (L.blocks + 1023) / 1024) * 4,  // 29 blkcnt + segment sums (tree.cu)
-      (size_t)L.cap_rec * 16,                  // 30 lvl_cm: fp32 com + bounding radius of each item
+      (size_t)L.cap_rec * 4,                   // 30 lvl_rad: bounding radius of each item (containment fold)
   };
   size_t off = 0;
   for (int i = 0; i < 31; i++) {
@@ -178,7 +178,7 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.lvl_mom = (double4 *)(b + L.off[27]);
   W.lvl_q = L.off[28] != L.off[29] ? (double *)(b + L.off[28]) : nullptr;
   W.blkcnt = (uint32_t *)(b + L.off[29]);
-  W.lvl_cm = (float4 *)(b + L.off[30]);
+  W.lvl_rad = (float *)(b + L.off[30]);
   W.redo = (uint32_t *)(b + L.off[21]);
   W.gcost = (uint32_t *)(b + L.off[22]);
   W.qmom = L.off[23] != L.off[24] ? (double *)(b + L.off[23]) : nullptr;

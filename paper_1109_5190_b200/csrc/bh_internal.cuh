@@ -134,7 +134,7 @@ struct Workspace {
   uint32_t *lvl_skip;   // skip() of the item's record
   double4 *lvl_mom;     // fp64 (M, MX, MY, MZ) of the item
   double *lvl_q;        // multipole = 2: fp64 quadrupole of the item (6 per item; null otherwise)
-  float4 *lvl_cm;       // (com32.xyz, bounding radius) of each item (containment folded into T_acc)
+  float *lvl_rad;       // bounding radius of each item about its com (containment folded into T_acc)
   DevStatus *status;
 };
 

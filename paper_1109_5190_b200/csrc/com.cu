@@ -31,7 +31,7 @@
 #include "bh_internal.cuh"
 
 #ifndef BH_MOM_PREFETCH
-#define BH_MOM_PREFETCH 4
+#define BH_MOM_PREFETCH 2  // (2 vs 1/3/4: best on cfg4 and on cfg5 with the containment fold)
 #endif
 #ifndef BH_MOM_MINB
 #define BH_MOM_MINB 0  // 0: no minimum-blocks bound
@@ -70,21 +70,22 @@ __device__ __forceinline__ void add_point_quad(double Q[6], double m, double y0,
 
 // Containment folded into the fp32 filter (theta >= 0.57 with eps > 0, so the
 // fast walk needs no per-visit containment test).  Every item carries a
-// bounding radius R about its fp32 com: R(particle) = 0, R(node) >= max over
-// children of |com - com32_child| + R_child (+ the child's com rounding), so
-// every particle of the node lies within R of its com, and a target inside the
-// node (one of its particles) is at distance <= R.  T_acc is raised to the
+// bounding radius R about its com: R(particle) = 0, R(node) >= max over
+// children of |com - com_child| + R_child (child coms from their fp64 moments,
+// with a reciprocal instead of a division and the rounding added), so every
+// particle of the node lies within R of its com, and a target inside the node
+// (one of its particles) is at distance <= R.  T_acc is raised to the
 // bound of R (the T_acc error model with r -> R): a node that may contain the
 // target is then never accepted for sure, and the band between T_rej and that
 // bound goes to the exact re-walk, which tests containment (reading L5).  For
 // most nodes R < s/theta already and nothing changes.
 struct ContFold {
-  float4 *lvl_cm;
+  float *lvl_rad;
   int on;
 };
 
 // one internal node of level `level` at item t (record c, children [lo, hi) of the next level)
-template <bool QUAD>
+template <bool QUAD, bool FOLD>
 __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, uint32_t lo, uint32_t hi, uint32_t off,
                                              uint32_t off1, double Ld, double theta,
                                              const uint32_t *__restrict__ item_rec, uint32_t *__restrict__ lvl_skip,
@@ -120,20 +121,48 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
   lvl_mom[off + t] = make_double4(M, X, Y, Z);
   lvl_skip[off + t] = skip;
   const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
-  const float fx = __double2float_rn(cx), fy = __double2float_rn(cy), fz = __double2float_rn(cz);
+  // a massless node has no com (0/0, as in the oracle): its record gets a finite
+  // dummy point and thresholds that always open it, so nothing NaN reaches the
+  // walk's branch-free arithmetic (0 x NaN)
+  const bool massless = !(M > 0.0);
+  const float fx = massless ? 0.f : __double2float_rn(cx), fy = massless ? 0.f : __double2float_rn(cy),
+              fz = massless ? 0.f : __double2float_rn(cz);
   double Rn = 0.0;
-  if (cf.on) {
-    // bounding radius: the children's fp32 coms and radii (their rounding, u |c|
-    // per axis, added)
-    for (uint32_t j = lo; j < hi; j++) {
-      const float4 q4 = cf.lvl_cm[off1 + j];
-      const double ex = cx - (double)q4.x, ey = cy - (double)q4.y, ez = cz - (double)q4.z;
-      const double r = sqrt(ex * ex + ey * ey + ez * ez) + (double)q4.w +
-                       6.0e-8 * (fabs((double)q4.x) + fabs((double)q4.y) + fabs((double)q4.z));
-      Rn = fmax(Rn, r);
-    }
-    Rn *= 1.0 + 1e-12;
-    cf.lvl_cm[off + t] = make_float4(fx, fy, fz, round_up_f(Rn));
+  if (FOLD) {
+    const double cn = fabs(cx) + fabs(cy) + fabs(cz);
+    // one child's reach |com - com_j| + R_j (+ rounding); a massless child: a
+    // particle's position from its record, a massless node unbounded
+    auto reach = [&](const double4 mj, float rj, uint32_t j) -> double {
+      if (mj.x > 1e-30) {
+        // |com - com_j| = |M_j com - MX_j| / M_j: the difference in fp64 (one
+        // fma per axis, no cancellation loss), then fp32 (relative precision of
+        // the distance itself): <= 10 fp32 roundings, covered by 1e-6
+        const float e0 = (float)fma(mj.x, cx, -mj.y), e1 = (float)fma(mj.x, cy, -mj.z),
+                    e2 = (float)fma(mj.x, cz, -mj.w);
+        const float d = sqrtf(fmaf(e2, e2, fmaf(e1, e1, e0 * e0))) / (float)mj.x;
+        return (double)d * (1.0 + 1e-6) + (double)rj;
+      }
+      double px, py, pz;
+      if (mj.x > 0.0) {  // (tiny masses: the slow exact route)
+        px = mj.y / mj.x;
+        py = mj.z / mj.x;
+        pz = mj.w / mj.x;
+      } else {  // massless: a particle's position from its record; a node unbounded
+        const uint32_t ec = item_rec[off1 + j];
+        if (!(ec & ITEM_LEAF)) return INFINITY;
+        const float4 pp = rec[ec & ~ITEM_LEAF].cm;
+        px = pp.x;
+        py = pp.y;
+        pz = pp.z;
+      }
+      const double ex = cx - px, ey = cy - py, ez = cz - pz;
+      const double d = sqrt(ex * ex + ey * ey + ez * ez);
+      return d + (double)rj + 1e-14 * (cn + fabs(px) + fabs(py) + fabs(pz) + d);
+    };
+    // the children again (just read for the sums: cached)
+    for (uint32_t j = lo; j < hi; j++) Rn = fmax(Rn, reach(lvl_mom[off1 + j], cf.lvl_rad[off1 + j], j));
+    if (!(Rn <= 1e300)) Rn = INFINITY;  // (also a NaN com of a massless node)
+    cf.lvl_rad[off + t] = Rn == INFINITY ? INFINITY : round_up_f(Rn * (1.0 + 1e-12));
   }
   if (QUAD) {
     // the quadrupole about (cx, cy, cz): the children in digit order, each its
@@ -161,12 +190,17 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     }
     // the walk's copy is -Q in fp32 (walk.cu: the minus sign of the field's
     // first term rides on Q, exactly)
-    qrec[2 * (size_t)c] = make_float4(-__double2float_rn(Q[0]), -__double2float_rn(Q[1]),
-                                      -__double2float_rn(Q[2]), -__double2float_rn(Q[3]));
-    qrec[2 * (size_t)c + 1] = make_float4(-__double2float_rn(Q[4]), -__double2float_rn(Q[5]), 0.f, 0.f);
+    if (massless) {
+      qrec[2 * (size_t)c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      qrec[2 * (size_t)c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      qrec[2 * (size_t)c] = make_float4(-__double2float_rn(Q[0]), -__double2float_rn(Q[1]),
+                                        -__double2float_rn(Q[2]), -__double2float_rn(Q[3]));
+      qrec[2 * (size_t)c + 1] = make_float4(-__double2float_rn(Q[4]), -__double2float_rn(Q[5]), 0.f, 0.f);
+    }
   }
   float tacc, trej;
-  if (!(theta > 0.0)) {
+  if (!(theta > 0.0) || massless) {
     tacc = INFINITY;
     trej = INFINITY;
   } else {
@@ -189,12 +223,12 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     // these cells in the fp32 filter routes every such decision to the exact
     // re-walk, which tests containment.
     if (level >= 20) tacc = INFINITY;
-    if (cf.on && level < 20) {
+    if (FOLD && level < 20) {
       const double u = 5.9604644775390625e-08;
       const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
       const double a = 1.5 * u, b = 1.5 * u * C, g = 4.5 * u;
       const double A = (Rn * (1.0 + 1e-12) + b) / (1.0 - a);
-      tacc = fmaxf(tacc, round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15)));
+      tacc = Rn == INFINITY ? INFINITY : fmaxf(tacc, round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15)));
     }
   }
   Rec r;
@@ -204,7 +238,7 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
   rec[c] = r;
 }
 
-template <bool QUAD>
+template <bool QUAD, bool FOLD>
 __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__restrict__ st,
                                                        const uint32_t *__restrict__ item_rec,
                                                        const uint32_t *__restrict__ item_clo,
@@ -243,7 +277,7 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
     lo = lon;
     hi = hin;
     if (ecur & ITEM_LEAF) continue;  // a particle: K4 wrote its record and moments
-    moments_node<QUAD>(level, t, ecur, locur, hicur, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec,
+    moments_node<QUAD, FOLD>(level, t, ecur, locur, hicur, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec,
                        lvl_q, qmom, qrec, cf, st);
   }
 }
@@ -252,7 +286,7 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
 cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont_fold, cudaStream_t s,
                            int *launches) {
   ContFold cf;
-  cf.lvl_cm = W.lvl_cm;
+  cf.lvl_rad = W.lvl_rad;
   cf.on = cont_fold;
   if (n < 2) return cudaSuccess;
   // grid: enough blocks for the widest level (at most n items), capped at 8
@@ -262,12 +296,17 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont
   int grid = (int)(need < lim ? need : lim);
   if (grid < 1) grid = 1;
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
-    if (W.qmom)
-      k_moments_level<true><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom, W.rec,
-                                                 theta, W.lvl_q, W.qmom, W.qrec, cf);
-    else
-      k_moments_level<false><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom,
-                                                  W.rec, theta, W.lvl_q, W.qmom, W.qrec, cf);
+#define BH_MOM_LAUNCH(Q, F)                                                                                  \
+  k_moments_level<Q, F><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom, W.rec, \
+                                             theta, W.lvl_q, W.qmom, W.qrec, cf)
+    if (W.qmom) {
+      if (cf.on) BH_MOM_LAUNCH(true, true);
+      else BH_MOM_LAUNCH(true, false);
+    } else {
+      if (cf.on) BH_MOM_LAUNCH(false, true);
+      else BH_MOM_LAUNCH(false, false);
+    }
+#undef BH_MOM_LAUNCH
     if (launches) (*launches)++;
   }
   return cudaGetLastError();

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
                                               const uint32_t *__restrict__ blkoff,
                                               int64_t nblk, const uint32_t *__restrict__ segoff, int64_t nseg,
                                               uint32_t *__restrict__ item_rec, uint32_t *__restrict__ rec_item,
-                                              float4 *__restrict__ lvl_cm, int cont_fold,
+                                              float *__restrict__ lvl_rad, int cont_fold,
                                               uint32_t *__restrict__ item_clo, uint32_t *__restrict__ lvl_skip,
                                               double4 *__restrict__ lvl_mom, float4 *__restrict__ qrec) {
   __shared__ uint16_t s_pre[BH_NLEVELS][256];
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
   lvl_skip[k] = c + 1u;
   const double m = (double)q.w;
   lvl_mom[k] = make_double4(m, __dmul_rn(m, (double)q.x), __dmul_rn(m, (double)q.y), __dmul_rn(m, (double)q.z));
-  if (cont_fold) lvl_cm[k] = make_float4(q.x, q.y, q.z, 0.f);  // a particle: its position, radius 0
+  if (cont_fold) lvl_rad[k] = 0.f;  // a particle: radius 0 about itself
   if (qrec) {  // multipole = 2: a particle has no quadrupole about itself
     qrec[2 * (size_t)c] = make_float4(0.f, 0.f, 0.f, 0.f);
     qrec[2 * (size_t)c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -270,7 +270,7 @@ cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf,
   k_level_scan_top<<<BH_NLEVELS, 1024, 0, s>>>(segsum, nseg, W.status);
   k_lvl_offsets<<<1, 32, 0, s>>>(W.nstart, n, cap_rec, W.status, W.rec, W.qrec);
   k_emit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.lcp, W.nstart, W.pos4, n,
-                                                     W.status, W.rec, W.blkcnt, nblk, segsum, nseg, W.item_rec, W.rec_item, cont_fold ? W.lvl_cm : nullptr, cont_fold,
+                                                     W.status, W.rec, W.blkcnt, nblk, segsum, nseg, W.item_rec, W.rec_item, cont_fold ? W.lvl_rad : nullptr, cont_fold,
                                                      W.item_clo, W.lvl_skip, W.lvl_mom, W.qrec);
   return cudaGetLastError();
 }
