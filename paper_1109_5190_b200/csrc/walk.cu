@@ -17,6 +17,9 @@ namespace bh {
 #ifndef BH_WALK2_BLOCK
 #define BH_WALK2_BLOCK 128
 #endif
+#ifndef BH_WALK2_UNROLL_SMALL
+#define BH_WALK2_UNROLL_SMALL 3  // visits per loop trip for groups of <= 2 lanes (3 vs 2: cfg5 -2.2%, cfg3 -1.2%, cfg2 -1.4%)
+#endif
 #ifndef BH_WALK2_MINB
 #define BH_WALK2_MINB 5
 #endif
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 && !QUAD ? BH_WALK2_M
   // (a parked group stays on the sentinel, so the extra visit is harmless)
   if (__any_sync(full, c < Wn)) for (;;) {
 #pragma unroll
-   for (int u = 0; u < BH_WALK2_UNROLL; u++) {
+   for (int u = 0; u < (GL <= 2 ? BH_WALK2_UNROLL_SMALL : BH_WALK2_UNROLL); u++) {
     const uint32_t cc = c;
     float4 cm;
     uint4 au;
