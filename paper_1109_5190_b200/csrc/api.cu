@@ -440,7 +440,7 @@ static bh_status build_tree(bh_ctx *ctx) {
   CK(launch_keys(ctx->W, n, s));
   CK(launch_sort(ctx->W, n, s, &buf));
   CK(launch_tie_fixup(ctx->W, n, buf, s));
-  prof_end(ctx, &pp, (ctx->near_sort ? 22 : 0) + 2 + SORT_PASSES + 1);
+  prof_end(ctx, &pp, (ctx->near_sort ? 22 : 0) + 3 + SORT_PASSES + 1);  // (+ the conditional zeroing kernel)
   ctx->sort_buf = buf;
   prof_begin(ctx, &pp, 2);
   CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, ctx->cont_fold, s));  // (zeroes the particles' quadrupoles)

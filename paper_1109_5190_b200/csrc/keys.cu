@@ -225,11 +225,23 @@ cudaError_t launch_keys_prev(const Workspace &W, int64_t n, uint32_t *flags, cud
   return cudaGetLastError();
 }
 
+// zero the full sort's histograms, tile counters and look-back status -- only
+// when it will run (the near-sorted path leaves st->near_ok set: nothing to do)
+__global__ void k_zero_unless_near(uint4 *__restrict__ p, int64_t n16, const DevStatus *__restrict__ st) {
+  if (st->near_ok) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 cudaError_t launch_keys(const Workspace &W, int64_t n, cudaStream_t s) {
   // zero histograms, tile counters and look-back status of all 8 passes
   int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
   size_t zero_bytes = sizeof(uint32_t) * (SORT_PASSES * SORT_RADIX + 8 + (size_t)SORT_PASSES * tiles * SORT_RADIX);
-  cudaError_t e = cudaMemsetAsync(W.sort_hist, 0, zero_bytes, s);
+  const int64_t n16 = (int64_t)((zero_bytes + 15) / 16);  // (the status area is 16-byte aligned and padded)
+  int64_t zg = (n16 + 255) / 256;
+  if (zg > 148 * 8) zg = 148 * 8;
+  k_zero_unless_near<<<(unsigned)zg, 256, 0, s>>>((uint4 *)W.sort_hist, n16, W.status);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int64_t need = (n + 255) / 256;
   int grid = (int)(need < 148 * 8 ? need : 148 * 8);

@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(SORT_BLOCK, 2) k_onesweep(const unsigned long 
   const uint32_t near = st->near_ok;
   if (mode == SORT_FULL ? near != 0u : near == 0u) return;  // uniform
   const int64_t n = mode == SORT_FULL ? n_arg : (int64_t)st->n_bad;
+  // exactly the blocks the data needs take a tile ticket (tickets 0 .. need-1
+  // all go out); the rest of a capacity-sized grid (SORT_BAD) leaves at once
+  const int64_t need = n > 0 ? (n + SORT_TILE - 1) / SORT_TILE : 1;
+  if ((int64_t)blockIdx.x >= need) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
   for (int i = tid; i < SORT_WARPS * SORT_RADIX; i += SORT_BLOCK) (&S.wcount[0][0])[i] = 0;
