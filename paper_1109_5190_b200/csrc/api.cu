@@ -439,8 +439,8 @@ static bh_status build_tree(bh_ctx *ctx) {
   if (ctx->near_sort) CK(launch_near_sort(ctx->W, n, s));
   CK(launch_keys(ctx->W, n, s));
   CK(launch_sort(ctx->W, n, s, &buf));
-  CK(launch_tie_fixup(ctx->W, n, buf, s));
-  prof_end(ctx, &pp, (ctx->near_sort ? 22 : 0) + 3 + SORT_PASSES + 1);  // (+ the conditional zeroing kernel)
+  // (equal keys are ordered by user index in K4's first kernel, k_lcp_count)
+  prof_end(ctx, &pp, (ctx->near_sort ? 22 : 0) + 2 + SORT_PASSES + 1);  // (+ zeroing, - tie fix-up)
   ctx->sort_buf = buf;
   prof_begin(ctx, &pp, 2);
   CK(launch_tree(ctx->W, n, ctx->lay.cap_rec, buf, ctx->cont_fold, s));  // (zeroes the particles' quadrupoles)

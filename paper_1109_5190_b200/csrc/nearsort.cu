@@ -21,7 +21,7 @@
 // (too many bad keys, or the good keys are not sorted) the full radix sort of
 // sort.cu runs instead (its kernels run only when near_ok is clear), so the
 // result is always the full sort's.  Equal keys end in some order and
-// k_tie_fixup re-sorts them by user index, as on the full path.
+// K4 (k_lcp_count) re-sorts them by user index, as on the full path.
 // HBM: K1' 32 B (+4 B flags), scan ~12 B, split 28 B, merge 24 B per key (+ the bad keys'
 // passes), against 32 + 192 B per key for K1 + the 8 full passes.
 #include "bh_internal.cuh"
