@@ -139,7 +139,9 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
         // the distance itself): <= 10 fp32 roundings, covered by 1e-6
         const float e0 = (float)fma(mj.x, cx, -mj.y), e1 = (float)fma(mj.x, cy, -mj.z),
                     e2 = (float)fma(mj.x, cz, -mj.w);
-        const float d = sqrtf(fmaf(e2, e2, fmaf(e1, e1, e0 * e0))) / (float)mj.x;
+        // (approximate sqrt and reciprocal: a few ulp, inside the 1e-6 margin)
+        const float q2 = fmaf(e2, e2, fmaf(e1, e1, e0 * e0));
+        const float d = q2 > 0.f ? q2 * rsqrtf(q2) * __frcp_rn((float)mj.x) : 0.f;
         return (double)d * (1.0 + 1e-6) + (double)rj;
       }
       double px, py, pz;
