@@ -26,6 +26,8 @@
 //   T_acc = RU(((r(1+delta) + b) / (1-a))^2 (1+g)),
 //   T_rej = RD(((r(1-delta) - b) / (1+a))^2 (1-g))   (or -inf if negative),
 // with a = 1.5u, b = 1.5u |c32|, g = 4.5u.  theta == 0: T_acc = T_rej = +inf.
+// For theta >= 0.57 T_acc is also raised to the bound of the node's bounding
+// radius, so the walk needs no containment test (ContFold below, reading R2).
 #include <math.h>
 
 #include "bh_internal.cuh"
