@@ -205,10 +205,18 @@ def ours_arm(args):
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
     comm = None
+    nccl_info = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
         uid = bdist.share_nccl_id(bhmod.nccl_unique_id, dist)
         comm = bhmod.nccl_comm_init(uid, world, rank, device)
+        nccl_info = bhmod.nccl_comm_info(comm)
+        print(f"rank {rank}: NCCL communicator spans {nccl_info['count']} ranks (this rank {nccl_info['rank']}, "
+              f"cuda:{nccl_info['device']})", file=sys.stderr, flush=True)
+        if nccl_info["count"] != world:
+            raise RuntimeError(f"NCCL communicator has {nccl_info['count']} ranks, WORLD_SIZE={world}")
+    else:
+        nccl_info = None
     cfg = bhgen.CONFIGS[args.config]
     m, p, v = bhgen.generate(cfg)
     prm = bhgen.params(cfg)
@@ -391,6 +399,7 @@ def ours_arm(args):
             "gpu_launches": int(launches),
             "ms_per_step_profiled_phases": sum(phase_ms.values()),
             "clocks": clocks,
+            "nccl": nccl_info,
             "ownership_balance": balance,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -404,7 +413,43 @@ def ours_arm(args):
     return 0
 
 
+def spawn_command(argv, gpus: int, port: int):
+    """The torchrun command that re-launches this script with one rank per GPU
+    (--gpus N without a torchrun environment): same arguments, 127.0.0.1
+    rendezvous."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_spawn(args, argv) -> int | None:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (one
+    process per GPU) and return its exit code; None when already a rank (or N = 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if args.impl == "ours":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"--gpus {args.gpus}: only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    cmd = spawn_command(argv, args.gpus, _free_port())
+    print("spawning: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -423,6 +468,9 @@ def main(argv=None):
     if args.warmup < 3 and args.impl == "ours":
         print("note: warm-up < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
+    rc = maybe_spawn(args, argv)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return reference_arm(args)
     return ours_arm(args)

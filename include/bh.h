@@ -253,6 +253,10 @@ const char *bh_status_string(int status);
  * (e.g. a torch.distributed broadcast). */
 bh_status bh_nccl_unique_id(void *id128);
 bh_status bh_nccl_comm_init(void **comm, const void *id128, int world, int rank, int device);
+/* The communicator's rank count, this rank and its CUDA device
+ * (ncclCommCount / ncclCommUserRank / ncclCommCuDevice; NULL outputs skipped).
+ * bench.py logs them so a run shows how many ranks NCCL actually spans. */
+bh_status bh_nccl_comm_info(void *comm, int *count, int *rank, int *device);
 bh_status bh_nccl_comm_destroy(void *comm);
 
 #ifdef __cplusplus

@@ -65,6 +65,7 @@ def lib():
         L.oracle_forces.argtypes = [vp, i64, vp, vp, vp]
         L.oracle_step.argtypes = [vp, i64, vp]
         L.oracle_get_state.argtypes = [vp, vp, vp]
+        L.oracle_step_targets.argtypes = [vp, i64, vp, vp, vp, vp]
         L.oracle_direct.argtypes = [i64, vp, vp, f64, f64, i64, vp, vp]
         L.oracle_set_multipole.argtypes = [vp, C.c_int]
         L.oracle_get_quadrupoles.restype = i64
@@ -174,6 +175,18 @@ class Oracle:
         inter = np.zeros(nsteps, np.int64)
         self._chk(lib().oracle_step(self._h, int(nsteps), _p(inter)))
         return inter
+
+    def step_targets(self, targets):
+        """One leapfrog step of the given user-index targets from the current
+        state, without advancing it: (pos[nt,3], vel[nt,3], interactions[nt])."""
+        t = np.ascontiguousarray(targets, dtype=np.int64)
+        nt = t.shape[0]
+        po = np.zeros((nt, 3), np.float64)
+        vo = np.zeros((nt, 3), np.float64)
+        cnt = np.zeros(nt, np.int64)
+        self._chk(lib().oracle_step_targets(self._h, nt, _p(t), _p(po), _p(vo), _p(cnt)))
+        self.built = True
+        return po, vo, cnt
 
     def state(self):
         p = np.zeros((self.n, 3), np.float64)

@@ -549,6 +549,41 @@ int oracle_forces(oracle_ctx *c, int64_t nt, const int64_t *targets, double *acc
     return OR_OK;
 }
 
+/* Leapfrog (L8) of one particle: k == 0: v += a dt/2, else v += a dt; then
+ * x += v dt (fp64). */
+static void leapfrog(const oracle_ctx *c, const double *x, const double *v, const double *a, double *xo,
+                     double *vo) {
+    double kick = (c->k == 0) ? 0.5 * c->dt : c->dt;
+    for (int d = 0; d < 3; d++) {
+        vo[d] = v[d] + a[d] * kick;
+        xo[d] = x[d] + vo[d] * c->dt;
+    }
+}
+
+/* One step of `nt` targets only (user indices), without changing the state:
+ * the tree of the current state (built if needed), the targets' forces, and
+ * their leapfrog update into pos_out / vel_out [nt][3].  The teacher-forced
+ * trajectory check of the large configurations: the oracle's step from the
+ * GPU's state at step k, on sampled particles (reading L24). */
+int oracle_step_targets(oracle_ctx *c, int64_t nt, const int64_t *targets, double *pos_out, double *vel_out,
+                        int64_t *count) {
+    if (nt < 0 || (nt > 0 && !targets)) return OR_ERR_ARG;
+    if (!c->built) {
+        int rc = oracle_build(c);
+        if (rc) return rc;
+    }
+    double *acc = (double *)malloc((size_t)(nt > 0 ? nt : 1) * 3 * sizeof(double));
+    if (!acc) return OR_ERR_OOM;
+    int rc = oracle_forces(c, nt, targets, acc, count);
+    if (rc == OR_OK)
+        for (int64_t t = 0; t < nt; t++) {
+            int64_t i = targets[t];
+            leapfrog(c, &c->pos[3 * i], &c->vel[3 * i], &acc[3 * t], &pos_out[3 * t], &vel_out[3 * t]);
+        }
+    free(acc);
+    return rc;
+}
+
 /* Leapfrog (L8): k == 0: v += a dt/2, else v += a dt; then x += v dt.  One
  * tree and one walk per step; velocities are staggered v_{k-1/2}. */
 int oracle_step(oracle_ctx *c, int64_t nsteps, int64_t *interactions) {
@@ -562,13 +597,9 @@ int oracle_step(oracle_ctx *c, int64_t nsteps, int64_t *interactions) {
         if (rc) break;
         rc = oracle_forces(c, 0, NULL, acc, cnt);
         if (rc) break;
-        double kick = (c->k == 0) ? 0.5 * c->dt : c->dt;
         int64_t tot = 0;
         for (int64_t i = 0; i < n; i++) {
-            for (int a = 0; a < 3; a++) {
-                c->vel[3 * i + a] = c->vel[3 * i + a] + acc[3 * i + a] * kick;
-                c->pos[3 * i + a] = c->pos[3 * i + a] + c->vel[3 * i + a] * c->dt;
-            }
+            leapfrog(c, &c->pos[3 * i], &c->vel[3 * i], &acc[3 * i], &c->pos[3 * i], &c->vel[3 * i]);
             tot += cnt[i];
         }
         if (interactions) interactions[st] = tot;

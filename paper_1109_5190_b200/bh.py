@@ -117,6 +117,7 @@ def load_library(path: str = LIB_PATH):
             "bh_nccl_unique_id": (i32, [vp]),
             "bh_nccl_comm_init": (i32, [C.POINTER(vp), vp, i32, i32, i32]),
             "bh_nccl_comm_destroy": (i32, [vp]),
+            "bh_nccl_comm_info": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -425,6 +426,16 @@ def nccl_comm_init(uid: bytes, world: int, rank: int, device: int):
     if rc != BH_OK:
         raise BhError(rc, "ncclCommInitRank failed")
     return comm
+
+
+def nccl_comm_info(comm) -> dict:
+    """{"count", "rank", "device"} of an NCCL communicator (bh_nccl_comm_info)."""
+    L = load_library()
+    cnt, rk, dev = C.c_int(0), C.c_int(0), C.c_int(0)
+    rc = L.bh_nccl_comm_info(comm, C.byref(cnt), C.byref(rk), C.byref(dev))
+    if rc != BH_OK:
+        raise BhError(rc, "ncclCommCount / UserRank / CuDevice failed")
+    return {"count": cnt.value, "rank": rk.value, "device": dev.value}
 
 
 def nccl_comm_destroy(comm):

@@ -790,7 +790,9 @@ static void drop_graphs(bh_ctx *ctx) {
 // data (every kernel reads its counts from the device), so it is captured once
 // per kick value into a CUDA graph and replayed: one launch per step instead of
 // ~45 (matters for the small configurations).  Not used while profiling (the
-// per-phase events) or for multi-rank communicators.
+// per-phase events).  With an NCCL communicator the grouped broadcast of K8 is
+// captured too (NCCL supports stream capture); bh_set_partition drops the
+// graphs, since the ranges are baked in.
 static bh_status step_graph(bh_ctx *ctx, int which, float kick, cudaGraphExec_t *out) {
   if (ctx->step_graph[which]) {
     *out = ctx->step_graph[which];
@@ -831,14 +833,24 @@ bh_status bh_step(bh_ctx *ctx, int nsteps) {
   }
   for (int k = 0; k < nsteps; k++) {
     // (a captured step must not contain bh_advance's one-off velocity load)
-    const bool graphs = ctx->use_graphs && !ctx->prof && !(ctx->p.world > 1 && ctx->p.nccl_comm) && !ctx->vel_pending;
+    // (with NCCL the captured step holds the grouped broadcast too; a capture
+    // the NCCL build refuses switches graphs off for this ctx: direct launches)
+    const bool graphs = ctx->use_graphs && !ctx->prof && !ctx->vel_pending;
     if (ctx->prof) ctx->prof_calls++;
     const int which = ctx->steps == 0 ? 0 : 1;
     const float kick = (float)(which == 0 ? 0.5 * ctx->p.dt : ctx->p.dt);
+    cudaGraphExec_t ge = nullptr;
     if (graphs) {
-      cudaGraphExec_t ge;
       st = step_graph(ctx, which, kick, &ge);
+      if (st && ctx->p.world > 1 && ctx->p.nccl_comm) {  // NCCL refused capture
+        cudaGetLastError();
+        ctx->use_graphs = 0;
+        ge = nullptr;
+        st = BH_OK;
+      }
       if (st) return st;
+    }
+    if (ge) {
       CK(cudaGraphLaunch(ge, ctx->stream));
       ctx->sort_buf = 0;  // 8 passes: the sorted keys end in buffer 0
     } else {
@@ -965,10 +977,18 @@ bh_status bh_advance(bh_ctx *ctx, const float *mass, const float *pos, const flo
     // own captured graph, the rest via bh_step
     if (ctx->prof) ctx->prof_calls++;
     const float kick = (float)(0.5 * ctx->p.dt);
-    if (ctx->use_graphs && !ctx->prof && !(ctx->p.world > 1 && ctx->p.nccl_comm)) {
-      cudaGraphExec_t ge;
+    cudaGraphExec_t ge = nullptr;
+    if (ctx->use_graphs && !ctx->prof) {
       st = step_graph(ctx, 2, kick, &ge);
+      if (st && ctx->p.world > 1 && ctx->p.nccl_comm) {  // NCCL refused capture
+        cudaGetLastError();
+        ctx->use_graphs = 0;
+        ge = nullptr;
+        st = BH_OK;
+      }
       if (st) return st;
+    }
+    if (ge) {
       CK(cudaGraphLaunch(ge, s));
       ctx->sort_buf = 0;
       ctx->vel_pending = false;
@@ -1300,6 +1320,25 @@ bh_status bh_nccl_comm_init(void **comm, const void *id128, int world, int rank,
   ncclComm_t c;
   if (ncclCommInitRank(&c, world, id, rank) != ncclSuccess) return BH_ERR_NCCL;
   *comm = (void *)c;
+  return BH_OK;
+}
+
+bh_status bh_nccl_comm_info(void *comm, int *count, int *rank, int *device) {
+  if (!comm) return BH_ERR_ARG;
+  ncclComm_t c = (ncclComm_t)comm;
+  int v;
+  if (count) {
+    if (ncclCommCount(c, &v) != ncclSuccess) return BH_ERR_NCCL;
+    *count = v;
+  }
+  if (rank) {
+    if (ncclCommUserRank(c, &v) != ncclSuccess) return BH_ERR_NCCL;
+    *rank = v;
+  }
+  if (device) {
+    if (ncclCommCuDevice(c, &v) != ncclSuccess) return BH_ERR_NCCL;
+    *device = v;
+  }
   return BH_OK;
 }
 

@@ -137,17 +137,22 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     auto reach = [&](const double4 mj, float rj, uint32_t j) -> double {
       if (mj.x > 1e-30) {
         // |com - com_j| = |M_j com - MX_j| / M_j: the difference in fp64 (one
-        // fma per axis, no cancellation loss), then fp32 (relative precision of
-        // the distance itself): <= 10 fp32 roundings, covered by 1e-6
+        // fma per axis, no cancellation loss), then fp32.  Error budget of d
+        // (relative, u = 2^-24): 3 conversions to fp32 (3u, on the squares 6u),
+        // the sum of squares (3u), rsqrtf (<= 2 ulp), q2 * rsqrt (u), the
+        // conversion of M_j and its reciprocal (2u), the last multiply (u):
+        // ~17u = 1.0e-6, covered by the factor (1 + 1.5e-6) below.
+        // An overflow of the fp32 difference (large masses: q2 = +inf, rsqrt 0,
+        // inf * 0 = NaN) or of d takes the fp64 route below instead -- a NaN
+        // must never reach the max over children.
         const float e0 = (float)fma(mj.x, cx, -mj.y), e1 = (float)fma(mj.x, cy, -mj.z),
                     e2 = (float)fma(mj.x, cz, -mj.w);
-        // (approximate sqrt and reciprocal: a few ulp, inside the 1e-6 margin)
         const float q2 = fmaf(e2, e2, fmaf(e1, e1, e0 * e0));
         const float d = q2 > 0.f ? q2 * rsqrtf(q2) * __frcp_rn((float)mj.x) : 0.f;
-        return (double)d * (1.0 + 1e-6) + (double)rj;
+        if (d < INFINITY) return (double)d * (1.0 + 1.5e-6) + (double)rj;
       }
       double px, py, pz;
-      if (mj.x > 0.0) {  // (tiny masses: the slow exact route)
+      if (mj.x > 0.0) {  // (tiny masses, or an fp32 overflow: the slow exact route)
         px = mj.y / mj.x;
         py = mj.z / mj.x;
         pz = mj.w / mj.x;
@@ -164,7 +169,11 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
       return d + (double)rj + 1e-14 * (cn + fabs(px) + fabs(py) + fabs(pz) + d);
     };
     // the children again (just read for the sums: cached)
-    for (uint32_t j = lo; j < hi; j++) Rn = fmax(Rn, reach(lvl_mom[off1 + j], cf.lvl_rad[off1 + j], j));
+    // (NaN-propagating max: fmax would drop a NaN reach)
+    for (uint32_t j = lo; j < hi; j++) {
+      const double rj = reach(lvl_mom[off1 + j], cf.lvl_rad[off1 + j], j);
+      Rn = (rj > Rn || rj != rj) ? rj : Rn;
+    }
     if (!(Rn <= 1e300)) Rn = INFINITY;  // (also a NaN com of a massless node)
     cf.lvl_rad[off + t] = Rn == INFINITY ? INFINITY : round_up_f(Rn * (1.0 + 1e-12));
   }

@@ -10,4 +10,4 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
-    config.addinivalue_line("markers", "slow: CPU test taking more than ~20 s")
+    config.addinivalue_line("markers", "slow: long test (CPU tests over ~20 s; the BH_SLOW=1 full free-running GPU run)")

@@ -481,3 +481,76 @@ def test_quadrupole_theta0_is_direct_and_counts_unchanged():
     c1 = oracle.Oracle(m, pd, theta=0.5, eps=1e-3).build().forces()[1]
     c2 = oracle.Oracle(m, pd, theta=0.5, eps=1e-3, multipole=2).build().forces()[1]
     assert np.array_equal(c1, c2)
+
+
+@pytest.mark.parametrize("eps_over_d", [0.05, 0.3, 1.0])
+@pytest.mark.parametrize("G", [1.0, 2.5])
+def test_softened_cell_field_is_minus_grad_potential(eps_over_d, G):
+    """Reading L25 at eps > 0: an accepted cell's field is -grad of the softened
+    potential Phi(x) = -G [M / r_e + (1/2) r^T Q r / r_e^5],  r = x - com,
+    r_e^2 = |r|^2 + eps^2 (the monopole + quadrupole terms of the Plummer-
+    softened cell, PAPER.md:755-757 future work "multipole moments").  The
+    potential is evaluated here from its definition (M, com, Q summed from the
+    particles in this test), differentiated by central differences, and
+    compared with the oracle's contribute_cell for a target that accepts the
+    cluster as one cell.  A wrong eps placement (r instead of r_e in inv5 /
+    inv7), a wrong factor or sign fails at eps ~ d (the quadrupole term is
+    ~1e-3 of the monopole's here, the tolerance 1e-9 of |a|)."""
+    rng = np.random.default_rng(5)
+    cl = rng.uniform(0.0, 1.0, (6, 3))
+    mc = rng.uniform(0.5, 2.0, 6)
+    d = 12.0
+    tgt = 0.5 + np.array([1.0, 0.7, 0.4]) / np.linalg.norm([1.0, 0.7, 0.4]) * d
+    m = np.concatenate([mc, [1.0]])
+    p = np.concatenate([cl, [tgt]])
+    eps = eps_over_d * d
+    o2 = oracle.Oracle(m, p, theta=0.9, eps=eps, G=G, multipole=2).build()
+    acc, cnt = o2.forces(np.array([6]))
+    assert cnt[0] == 1  # the cluster is one accepted cell
+    # the cell's moments from the particles (not from the oracle)
+    M = mc.sum()
+    com = (mc[:, None] * cl).sum(0) / M
+    y = cl - com
+    Q = np.einsum("k,ki,kj->ij", mc, 3.0 * y, y) - np.eye(3) * (mc * (y * y).sum(1)).sum()
+
+    def phi(x):
+        r = x - com
+        re2 = r @ r + eps * eps
+        return -G * (M / np.sqrt(re2) + 0.5 * (r @ Q @ r) / re2 ** 2.5)
+
+    def grad(f, x, h=1e-3):  # fourth-order central differences
+        return np.array([(8 * (f(x + h * e) - f(x - h * e)) - (f(x + 2 * h * e) - f(x - 2 * h * e))) / (12 * h)
+                         for e in np.eye(3)])
+
+    ref = -grad(phi, tgt)
+    assert np.linalg.norm(acc[0] - ref) <= 1e-9 * np.linalg.norm(ref), (acc[0], ref)
+    # and the quadrupole part alone (oracle multipole 2 minus multipole 1) against
+    # -grad of the quadrupole term: it is not lost under the monopole's size
+    a1, _ = oracle.Oracle(m, p, theta=0.9, eps=eps, G=G).build().forces(np.array([6]))
+
+    def phiq(x):
+        r = x - com
+        re2 = r @ r + eps * eps
+        return -G * 0.5 * (r @ Q @ r) / re2 ** 2.5
+
+    gq = -grad(phiq, tgt)
+    assert np.linalg.norm((acc[0] - a1[0]) - gq) <= 1e-6 * np.linalg.norm(gq), (acc[0] - a1[0], gq)
+
+
+def test_step_targets_equals_full_step():
+    """oracle_step_targets (the teacher-forced check of the large configs) is the
+    pinned leapfrog of oracle_step restricted to the targets: bitwise equal at
+    k = 0 (half kick) and k = 1 (full kick), and the state is not advanced."""
+    m, p, v = bhgen.generate("cfg2", n=3000)
+    prm = bhgen.params("cfg2")
+    tg = np.array([0, 5, 17, 999, 2999])
+    for k0 in (0, 1):
+        o = oracle.Oracle(m, p.astype(np.float64), v.astype(np.float64), k0=k0, **prm)
+        po, vo, cnt = o.step_targets(tg)
+        p0, v0 = o.state()
+        assert np.array_equal(p0, p.astype(np.float64))  # not advanced
+        o.step(1)
+        p1, v1 = o.state()
+        assert np.array_equal(po, p1[tg]) and np.array_equal(vo, v1[tg])
+        o2 = oracle.Oracle(m, p.astype(np.float64), v.astype(np.float64), k0=k0, **prm).build()
+        assert np.array_equal(cnt, o2.forces(tg)[1])
