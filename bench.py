@@ -371,14 +371,14 @@ def ours_arm(args):
             "config": dict(workload_config(cfg, m, p, v), parallelism=f"morton-range x{world}",
                            multipole=args.multipole,
                            walk_group=args.walk_group,
-                           walk_kernel=(("k_walk2<4,1>: 8-target groups, 4 lanes x 2 targets"
+                           walk_kernel=(("k_walk<4>: 8-target groups, 4 lanes x 2 targets"
                                          if cfg.theta < 0.6 and cfg.n >= (1 << 22)
-                                         else "k_walk2<2,1>: 4-target groups, 2 lanes x 2 targets")
+                                         else "k_walk<2>: 4-target groups, 2 lanes x 2 targets")
                                         if args.walk_group == 0 else f"walk_group {args.walk_group} (include/bh.h)")),
             "particles_per_s": particles_per_s,
             "interactions_per_step": inter / args.steps,
             "fp32_peak_frac": achieved_tf / peak,
-            "roofline": {"bound": "alu", "kernel": "K6+K7 walk phase: k_walk2 + k_walk_resume", "achieved": achieved_tf,
+            "roofline": {"bound": "alu", "kernel": "K6+K7 walk phase: k_walk + k_walk_resume", "achieved": achieved_tf,
                          "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak, "traffic": traffic,
                          "traffic_source": traffic_src,

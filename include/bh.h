@@ -78,20 +78,16 @@ typedef struct {
     int64_t node_capacity; /* tree records (internal nodes + particles); 0 = default
                               (n + max(n, min(21 n, 2^22)) + 64, which always fits
                               n <= 199,728 and typical inputs above that)              */
-    int walk_group;     /* force-walk variant; every value gives bitwise-identical results:
-                           0 = automatic: packed fp32, 2 targets per lane, 2 lanes share one
-                           traversal (4-target groups, code 68), or 4 lanes (8-target groups,
-                           code 67) when theta < 0.6 and n >= 2^22; 1, 2, 4, 8, 16, 32 = one target per
-                           lane, that many lanes per traversal; 64..70 = packed variants
-                           (64: 32 lanes x 2, 65/69/70: 8/4/2 lanes x 4, 66/67/68: 8/4/2 lanes x 2);
-                           80..85 = persistent lane groups (80: 1 x 4, 81: 1 x 2, 82: 2 x 4,
-                           83: 2 x 2, 84: 4 x 2, 85: 4 x 4 lanes x targets), 90..95 = the same
-                           groups without persistence (one group per slot)                 */
+    int walk_group;     /* force-walk group size: 0 = automatic (code 68: 2 lanes x 2 targets share
+                           one traversal, 4-target groups; code 67: 4 lanes, 8-target groups,
+                           when theta < 0.6 and n >= 2^22); 66 / 67 / 68 = 8 / 4 / 2 lanes x 2
+                           targets.  Interaction counts never depend on it; the fp32 block sums
+                           of a target follow its group's walk, so forces agree to rounding
+                           across codes and bitwise for one code at any rank count       */
     int multipole;      /* cell expansion: 0 or 1 = monopole (the paper's method); 2 = monopole
                            + traceless quadrupole about the cell's centre of mass (the paper's
                            future work; reading L25 of DESIGN.md §3).  The MAC
-                           and the interaction counts do not change; with 2, walk_group must be
-                           0, 1-32 or 64-70                                                    */
+                           and the interaction counts do not change                         */
 } bh_params;
 
 /* Bytes of device workspace the ctx needs for these params (n, world,
@@ -221,7 +217,7 @@ typedef struct {
     int64_t opens;          /* last walk: MAC tests that opened a node             */
     int64_t interactions_cum; /* all walks since bh_create                        */
     int64_t opens_cum;
-    int64_t lane_iters;     /* last walk: traversal-loop iterations x lanes (SIMD slots) */
+    int64_t lane_iters;     /* reserved (0)                                              */
     int64_t redo_targets;   /* last walk: targets whose fp32 MAC test was inconclusive,
                                continued with the exact fp64 test (k_walk_resume)        */
     int64_t near_sorted;    /* last build: 1 if the sort took the near-sorted path (keys
@@ -237,13 +233,10 @@ bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);
 bh_status bh_set_profiling(bh_ctx *ctx, int enable);
 bh_status bh_get_profile(bh_ctx *ctx, double *ms, int64_t *launches, int64_t *calls);
 
-/* Walk statistics (opens, lane_iters of bh_get_stats) cost a few instructions
- * per visited node; they are off by default (interactions are always counted). */
+/* Walk statistics (the opens of bh_get_stats: MAC tests that opened a node)
+ * cost a few instructions per visited node; they are off by default
+ * (interactions are always counted). */
 bh_status bh_set_walk_stats(bh_ctx *ctx, int enable);
-/* Per record level 0..22 (22 = bucket members), accumulated over stats-mode
- * walks since bh_set_walk_stats(ctx, 1): SIMD slots, active lane-visits and
- * interactions; arrays of 24 (any may be NULL). */
-bh_status bh_get_walk_level_stats(bh_ctx *ctx, int64_t *iters24, int64_t *active24, int64_t *inter24);
 
 const char *bh_last_error(const bh_ctx *ctx);
 const char *bh_status_string(int status);

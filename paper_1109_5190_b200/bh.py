@@ -110,7 +110,6 @@ def load_library(path: str = LIB_PATH):
             "bh_get_stats": (i32, [vp, C.POINTER(BhStats)]),
             "bh_set_profiling": (i32, [vp, i32]),
             "bh_set_walk_stats": (i32, [vp, i32]),
-            "bh_get_walk_level_stats": (i32, [vp, vp, vp, vp]),
             "bh_get_profile": (i32, [vp, vp, vp, vp]),
             "bh_last_error": (C.c_char_p, [vp]),
             "bh_status_string": (C.c_char_p, [i32]),
@@ -370,11 +369,6 @@ class BarnesHut:
 
     def set_walk_stats(self, on=True):
         self._chk(self.L.bh_set_walk_stats(self.h, 1 if on else 0))
-
-    def get_walk_level_stats(self):
-        it, ac, ia = (np.zeros(24, np.int64) for _ in range(3))
-        self._chk(self.L.bh_get_walk_level_stats(self.h, _ptr(it), _ptr(ac), _ptr(ia)))
-        return it, ac, ia
 
     def set_profiling(self, on=True):
         self._chk(self.L.bh_set_profiling(self.h, 1 if on else 0))

@@ -105,7 +105,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
   L.blocks = (n + 1 + 255) / 256;  // tree.cu's particle blocks
-  size_t sz[31] = {
+  size_t sz[32] = {
       sizeof(DevStatus),                       // 0 status
       (size_t)n * 16,                          // 1 pos4
       (size_t)L.n_own_max * 16,                // 2 vel4
@@ -137,9 +137,10 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
       multipole == 2 ? (size_t)L.cap_rec * 48 : 0,  // 28 lvl_q
       (size_t)BH_NLEVELS * (L.blocks + (L.blocks + 1023) / 1024) * 4,  // 29 blkcnt + segment sums (tree.cu)
       (size_t)L.cap_rec * 4,                   // 30 lvl_rad: bounding radius of each item (containment fold)
+      (size_t)BH_NLEVELS * ((n + 4095) / 4096 + 1) * 4,  // 31 K5 straggler queues (com.cu, MOM_CHUNK 4096)
   };
   size_t off = 0;
-  for (int i = 0; i < 31; i++) {
+  for (int i = 0; i < 32; i++) {
     L.off[i] = off;
     off += align_up(sz[i]);
   }
@@ -181,6 +182,7 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.lvl_rad = (float *)(b + L.off[30]);
   W.redo = (uint32_t *)(b + L.off[21]);
   W.gcost = (uint32_t *)(b + L.off[22]);
+  W.mom_strag = (uint32_t *)(b + L.off[31]);
   W.qmom = L.off[23] != L.off[24] ? (double *)(b + L.off[23]) : nullptr;
   W.qrec = L.off[24] != L.off[25] ? (float4 *)(b + L.off[24]) : nullptr;
 }
@@ -293,30 +295,6 @@ __global__ void k_scatter1(uint32_t *__restrict__ out, const uint32_t *__restric
   if (s < hi) out[uid[s]] = src[s];
 }
 
-// owned targets: flags then compaction of the sorted positions whose storage id is own
-__global__ void k_own_flags(const uint32_t *__restrict__ vals, uint32_t *__restrict__ flag, int64_t n, uint32_t lo,
-                            uint32_t hi) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p < n) { uint32_t s = vals[p]; flag[p] = (s >= lo && s < hi) ? 1u : 0u; }
-  if (p == n) flag[n] = 0;
-}
-__global__ void k_own_compact(const uint32_t *__restrict__ vals, const uint32_t *__restrict__ pre,
-                              uint32_t *__restrict__ targets, int64_t n, uint32_t lo, uint32_t hi) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p < n) { uint32_t s = vals[p]; if (s >= lo && s < hi) targets[pre[p]] = (uint32_t)p; }
-}
-
-cudaError_t launch_own_targets(const Workspace &W, int64_t n, int buf, uint32_t lo, uint32_t hi, cudaStream_t s) {
-  // flags live in accu (n + 1 u32 fit in 3n floats for n >= 1)
-  uint32_t *flag = (uint32_t *)W.accu;
-  unsigned g = (unsigned)((n + 1 + 255) / 256);
-  k_own_flags<<<g, 256, 0, s>>>(W.vals[buf], flag, n, lo, hi);
-  cudaError_t e = launch_scan_u32(flag, n + 1, W.scan_tmp, s);
-  if (e != cudaSuccess) return e;
-  k_own_compact<<<g, 256, 0, s>>>(W.vals[buf], flag, W.targets, n, lo, hi);
-  return cudaGetLastError();
-}
-
 }  // namespace bh
 
 // ---------------------------------------------------------------- helpers
@@ -341,14 +319,9 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     snprintf(err, errn, "multipole must be 0, 1 or 2");
     return BH_ERR_ARG;
   }
-  if (p->multipole == 2 && p->walk_group >= 80) {
-    snprintf(err, errn, "multipole = 2 needs walk_group 0, 1-32 or 64-70");
-    return BH_ERR_ARG;
-  }
   int g = p->walk_group;
-  if (!(g == 0 || g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32 || (g >= 64 && g <= 70) ||
-        (g >= 80 && g <= 85) || (g >= 90 && g <= 95))) {
-    snprintf(err, errn, "walk_group must be 0, 1, 2, 4, 8, 16, 32, 64..70, 80..85 or 90..95");
+  if (!(g == 0 || g == 66 || g == 67 || g == 68)) {
+    snprintf(err, errn, "walk_group must be 0 (automatic), 66, 67 or 68");
     return BH_ERR_ARG;
   }
   return BH_OK;
@@ -483,18 +456,14 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.theta2 = ctx->p.theta * ctx->p.theta;
   a.quad = ctx->p.multipole == 2;
   a.own_lo = (uint32_t)ctx->own_lo;
+  a.own_hi = (uint32_t)ctx->own_hi;
   a.acc_out = mode == 0 ? acc_out : nullptr;
   a.user_order = user_order ? 1 : 0;
   CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 6 * sizeof(unsigned long long), s));
-  if (ctx->p.world > 1) {
-    CK(launch_own_targets(ctx->W, n, ctx->sort_buf, (uint32_t)ctx->own_lo, (uint32_t)ctx->own_hi, s));
-    a.use_targets = 1;
-    a.n_targets = ctx->own_hi - ctx->own_lo;
-    launches += 4;
-  } else {
-    a.use_targets = 0;
-    a.n_targets = n;
-  }
+  // world > 1: the rank walks the P = 1 groups that hold one of its particles
+  // (every target summed in the same group as at P = 1: bitwise equal results)
+  a.own_check = ctx->p.world > 1 ? 1 : 0;
+  if (a.own_check) launches += 4;
   CK(launch_walk(ctx->W, a, s));
   prof_end(ctx, &pp, launches);
   ctx->walked = true;
@@ -1038,6 +1007,26 @@ bh_status bh_get_keys(bh_ctx *ctx, uint64_t *keys, uint32_t *perm) {
   return do_sync(ctx);
 }
 
+// Level (0 .. 22; 22 = bucket member) and leaf flag of every record, from the
+// level-ordered items of K4 (record -> item -> the level whose item range holds
+// it; leaf = the item is a particle's own record).  Host side, inspection only.
+static bh_status record_levels(bh_ctx *ctx, uint32_t nrec, std::vector<uint8_t> &lev, std::vector<uint8_t> &leaf) {
+  std::vector<uint32_t> item(nrec), irec(nrec);
+  CK(cudaMemcpy(item.data(), ctx->W.rec_item, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(irec.data(), ctx->W.item_rec, (size_t)nrec * 4, cudaMemcpyDeviceToHost));
+  lev.assign(nrec, 0);
+  leaf.assign(nrec, 0);
+  const uint32_t *off = ctx->hstatus->lvl_offset;
+  for (uint32_t c = 0; c < nrec; c++) {
+    const uint32_t it = item[c];
+    int l = 0;
+    while (l + 1 < BH_NLEVELS && off[l + 1] <= it) l++;
+    lev[c] = (uint8_t)l;
+    leaf[c] = (irec[it] & ITEM_LEAF) ? 1 : 0;
+  }
+  return BH_OK;
+}
+
 static bh_status export_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint32_t *count, double *M, double *MX,
                              int64_t cap, int64_t *n_nodes) {
   // copy the raw records back and re-format on the host (inspection only):
@@ -1067,13 +1056,16 @@ static bh_status export_tree(bh_ctx *ctx, uint8_t *level, uint32_t *first, uint3
     CK(cudaMemcpy(lm.data(), ctx->W.lvl_mom, (size_t)nrec * 32, cudaMemcpyDeviceToHost));
     for (uint32_t c = 0; c < nrec; c++) mom[c] = lm[item[c]];
   }
+  std::vector<uint8_t> lev, leafv;
+  st = record_levels(ctx, nrec, lev, leafv);
+  if (st) return st;
   int64_t k = 0;
   for (uint32_t c = 0; c < nrec; c++) {
     const uint4 a = rec[c].aux;
-    if (a.w & META_MEMBER) continue;
+    if (lev[c] > BH_MAXLEVEL) continue;  // a bucket member (level 22) is not a node of the export
     if (k < cap) {
-      const bool leaf = (a.w & META_LEAF) != 0;
-      if (level) level[k] = (uint8_t)(a.w & META_LEVEL_MASK);
+      const bool leaf = leafv[c] != 0;
+      if (level) level[k] = lev[c];
       if (first) first[k] = fst[c];
       if (count) count[k] = leaf ? 1u : (uint32_t)((a.z >= nrec ? (uint32_t)n : fst[a.z]) - fst[c]);
       if (M || MX) {
@@ -1122,12 +1114,14 @@ bh_status bh_get_quadrupoles(bh_ctx *ctx, double *Q, int64_t cap, int64_t *n_nod
   std::vector<double> q((size_t)nrec * 6);
   CK(cudaMemcpy(rec.data(), ctx->W.rec, (size_t)nrec * sizeof(Rec), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(q.data(), ctx->W.qmom, (size_t)nrec * 48, cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> lev, leafv;
+  st = record_levels(ctx, nrec, lev, leafv);
+  if (st) return st;
   int64_t k = 0;
   for (uint32_t c = 0; c < nrec; c++) {
-    const uint4 a = rec[c].aux;
-    if (a.w & META_MEMBER) continue;
+    if (lev[c] > BH_MAXLEVEL) continue;  // bucket member
     if (Q && k < cap)
-      for (int j = 0; j < 6; j++) Q[6 * k + j] = (a.w & META_LEAF) ? 0.0 : q[6 * (size_t)c + j];
+      for (int j = 0; j < 6; j++) Q[6 * k + j] = leafv[c] ? 0.0 : q[6 * (size_t)c + j];
     k++;
   }
   if (n_nodes) *n_nodes = k;
@@ -1282,25 +1276,6 @@ bh_status bh_set_walk_stats(bh_ctx *ctx, int enable) {
   if (!ctx) return BH_ERR_ARG;
   ctx->walk_stats = enable ? 1 : 0;
   drop_graphs(ctx);  // the captured steps bake in the walk variant
-  if (enable) {
-    bh_status st = set_dev(ctx);
-    if (st) return st;
-    CK(cudaMemsetAsync(ctx->W.status->lvl_iters, 0, 3 * 24 * sizeof(unsigned long long), ctx->stream));
-  }
-  return BH_OK;
-}
-
-bh_status bh_get_walk_level_stats(bh_ctx *ctx, int64_t *iters24, int64_t *active24, int64_t *inter24) {
-  if (!ctx) return BH_ERR_ARG;
-  bh_status st = set_dev(ctx);
-  if (st) return st;
-  st = do_sync(ctx);
-  if (st) return st;
-  for (int l = 0; l < 24; l++) {
-    if (iters24) iters24[l] = (int64_t)ctx->hstatus->lvl_iters[l];
-    if (active24) active24[l] = (int64_t)ctx->hstatus->lvl_active[l];
-    if (inter24) inter24[l] = (int64_t)ctx->hstatus->lvl_inter[l];
-  }
   return BH_OK;
 }
 

@@ -13,7 +13,9 @@
 //                     has exactly one record (a single-particle leaf, or a
 //                     "member" record right after its level-21 bucket):
 //                       rec[c].cm  float4 (com32.xyz, M32)       16 B
-//                       rec[c].aux uint4  (T_acc, T_rej, skip, meta) 16 B
+//                       rec[c].aux uint4  (T_acc, T_rej, skip, drop word) 16 B
+//                       (drop word = BH_DROP | c: the walk's resume word of
+//                       a target whose MAC test at c was inconclusive)
 //                       (one 32-byte sector per record: a lane's visit
 //                       touches one sector)
 //                     skip(c) = index of the first record after c's subtree,
@@ -35,13 +37,6 @@
 
 namespace bh {
 
-// meta bits of rec[c].aux.w
-enum : uint32_t {
-  META_LEVEL_MASK = 0x1f,  // level 0..21; 22 for bucket members
-  META_LEAF = 1u << 5,     // single-particle leaf or bucket member (has no children)
-  META_MEMBER = 1u << 6,   // bucket member record (not a tree node of the export)
-  META_BUCKET = 1u << 7,   // level-21 node with >= 2 particles
-};
 #define ITEM_LEAF 0x80000000u  // item_rec flag: the item is a particle's own record
 
 // device status block (one per ctx, in the workspace)
@@ -62,8 +57,9 @@ struct DevStatus {
   unsigned long long opens;          // last walk: MAC tests that opened a node (incl. self leaf)
   unsigned long long iters;          // last walk: group-loop iterations summed over lanes
   unsigned long long n_redo;         // last walk: targets re-walked with the exact fp64 MAC
-  unsigned long long walk_next;      // last walk: next target group of the persistent lane walk
-  uint32_t sm_next[256];             // walk: next chunk of each SM's segment (zeroed per walk)
+  unsigned long long reserved0;
+  uint32_t n_own_groups;             // world > 1: walk groups holding an own particle (walk.cu)
+  uint32_t reserved1;
   uint32_t near_ok;     // this build's sort came from the near-sorted path (sort.cu)
   uint32_t n_bad;       // near-sorted path: keys out of local order, sorted apart
   unsigned long long interactions_cum;  // since create / set_state
@@ -72,13 +68,9 @@ struct DevStatus {
   float L;
   float scale;
   uint32_t pad[3];
+  uint32_t mom_strag[24];   // K5: non-local nodes queued per level (com.cu k_moments_local; zeroed by K4)
   uint32_t lvl_count[24];   // items (records) per level 0..22; [23] = 0
   uint32_t lvl_offset[24];  // exclusive prefix of lvl_count (level-ordered item arrays)
-  // walk statistics per record level (stats mode): group iterations, active
-  // lane-visits, interactions
-  unsigned long long lvl_iters[24];
-  unsigned long long lvl_active[24];
-  unsigned long long lvl_inter[24];
 };
 
 struct __align__(32) Rec {
@@ -95,10 +87,9 @@ struct __align__(32) Rec {
 // fp32 partial sums and count over the DFS prefix before cdrop (walk.cu
 // k_walk_resume continues the same DFS from there with the exact MAC)
 struct __align__(32) ResumeState {
-  float ax, ay, az;
+  double ax, ay, az;  // the fast walk's partial sums (fp32 blocks folded in fp64)
   uint32_t cnt;
   uint32_t cdrop;
-  uint32_t pad[3];
 };
 
 struct Workspace {
@@ -111,9 +102,10 @@ struct Workspace {
   uint32_t *nstart;   // n + 1
   uint32_t *icount;   // interactions per storage id
   float *accu;        // n * 3, user order (BH_HOST force output staging)
-  uint32_t *targets;  // own sorted positions (world > 1)
+  uint32_t *targets;  // world > 1: the walk groups holding an own particle (walk.cu)
   uint32_t *redo;     // target slots whose fp32 MAC filter was inconclusive
-  uint32_t *gcost;    // per storage id: union-walk trips of its k_walk2 group in the last walk
+  uint32_t *gcost;      // per storage id: loop trips of its walk group in the last walk (group order)
+  uint32_t *mom_strag;  // K5 straggler queues: [level][chunks + 1] item indices (com.cu)
   double *qmom;       // multipole = 2: per record, fp64 quadrupole xx yy zz xy xz yz (null otherwise)
   float4 *qrec;       // multipole = 2: per record, 2 float4 = fp32 (xx yy zz xy) (xz yz 0 0)
   uint32_t *scan_tmp; // scan tile partials
@@ -141,7 +133,7 @@ struct Workspace {
 struct Layout {
   int64_t n, cap_rec, cap_int, n_own_max, sort_tiles, scan_tiles, cap_resume, blocks;
   size_t total;
-  size_t off[32];
+  size_t off[33];
 };
 
 // radix sort geometry (sort.cu)
@@ -156,6 +148,7 @@ constexpr int SCAN_ITEMS = 16;
 constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
 
 constexpr int BBOX_BLOCKS = 592;  // 4 x 148 SMs
+constexpr int LS_SEG = 1024;      // tree.cu: 256-particle blocks per level-scan segment
 
 Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole);
 void bind_workspace(const Layout &L, void *base, Workspace &W);
@@ -176,11 +169,10 @@ cudaError_t launch_own_targets(const Workspace &W, int64_t n, int buf, uint32_t 
                                cudaStream_t s);
 
 struct WalkArgs {
-  int64_t n;            // particles
-  int64_t n_targets;    // targets walked (own count)
-  int use_targets;      // 1: targets[] holds sorted positions; 0: target t is sorted position t
+  int64_t n;            // particles (targets: sorted positions 0 .. n-1)
+  int own_check;        // world > 1: walk the P = 1 groups holding an own particle, write own results only
   int buf;              // sort buffer holding vals
-  int group;            // lanes per shared traversal
+  int group;            // walk_group code (66 / 67 / 68: 8 / 4 / 2 lanes per shared traversal)
   int stats;            // 1: also count opened nodes and SIMD slots
   int num_sms;
   int need_cont;        // 0: theta < 1/sqrt(3) and eps > 0 -> no cell containing the
@@ -190,10 +182,11 @@ struct WalkArgs {
   float kick, dt;       // mode 1
   double theta2;
   int quad;             // multipole = 2: add each accepted cell's quadrupole field
-  uint32_t own_lo;
+  uint32_t own_lo, own_hi;
   float *acc_out;       // mode 0: [n][3] device output (may be null)
   int user_order;       // 1: acc_out[uid[s]], 0: acc_out[s - own_lo]
 };
 cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s);
+int walk_lanes(int group);
 
 }  // namespace bh

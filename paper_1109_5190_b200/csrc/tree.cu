@@ -87,7 +87,6 @@ __global__ void __launch_bounds__(256) k_lcp_count(const unsigned long long *__r
 // k_level_scan_top: one thread block per level scans the segment totals in
 // place (-> segment offsets) and writes the level's item count.
 // Global rank base of particle block k at level l: blkcnt[l][k] + segsum[l][k / LS_SEG].
-constexpr int LS_SEG = 1024;
 __global__ void __launch_bounds__(256) k_level_scan_seg(uint32_t *__restrict__ blkcnt, int64_t nblk,
                                                         uint32_t *__restrict__ segsum, int64_t nseg) {
   __shared__ uint32_t wsum[8];
@@ -156,6 +155,7 @@ __global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, in
                               Rec *__restrict__ rec, float4 *__restrict__ qrec) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint32_t run = 0;
+  for (int l = 0; l < 24; l++) st->mom_strag[l] = 0;  // K5's straggler queues (com.cu)
   for (int l = 0; l < BH_NLEVELS; l++) {
     st->lvl_offset[l] = run;
     run += st->lvl_count[l];
@@ -172,7 +172,10 @@ __global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, in
     return;
   }
   rec[nrec].cm = make_float4(0.f, 0.f, 0.f, 0.f);
-  rec[nrec].aux = make_uint4(__float_as_uint(INFINITY), __float_as_uint(INFINITY), nrec, 0u);
+  // the walk's sentinel (walk.cu): T_acc = +inf, T_rej = -inf, skip = itself,
+  // drop word nrec + 1 -- a target parks there without dropping out, and the
+  // group never opens it
+  rec[nrec].aux = make_uint4(__float_as_uint(INFINITY), __float_as_uint(-INFINITY), nrec, nrec + 1u);
   if (qrec) {  // parked groups visit the sentinel: its quadrupole must be finite (zero)
     qrec[2 * (size_t)nrec] = make_float4(0.f, 0.f, 0.f, 0.f);
     qrec[2 * (size_t)nrec + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -250,13 +253,12 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
   }
   // the particle's own record: a leaf at level ll (<= 21) or a bucket member (22)
   const uint32_t c = base + (uint32_t)(b > a ? b - a : 0);
-  const uint32_t meta = ll <= BH_MAXLEVEL ? ((uint32_t)ll | META_LEAF)
-                                          : ((uint32_t)(BH_MAXLEVEL + 1) | META_LEAF | META_MEMBER);
   const float4 q = pos4[vals[p]];
   Rec r;
   r.cm = q;
-  // T_acc = -inf: a particle record is always "accepted" unless it is the target
-  r.aux = make_uint4(__float_as_uint(-INFINITY), __float_as_uint(-INFINITY), c + 1u, meta);
+  // T_acc = -inf: a particle record is always "accepted" unless it is the
+  // target; the fourth word is the walk's drop word BH_DROP | c
+  r.aux = make_uint4(__float_as_uint(-INFINITY), __float_as_uint(-INFINITY), c + 1u, BH_DROP | c);
   rec[c] = r;
   const uint32_t k = s_off[ll] + rk;
   item_rec[k] = c | ITEM_LEAF;

@@ -1,64 +1,123 @@
-// walk.cu -- K6 force walk (+ K7 fused leapfrog): the production kernel
-// k_walk2 and launch_walk.  Semantics, readings and the shared pieces:
-// walk_common.cuh.
+// walk.cu -- K6 force walk (+ K7 fused leapfrog): k_walk and launch_walk.
+// Semantics, readings and the shared pieces: walk_common.cuh.
+//
+// Every lane carries TWO targets and evaluates them with Blackwell's packed
+// fp32 instructions (FADD2 / FMUL2 / FFMA2: one issue slot, two fp32 results;
+// the record's fields enter as broadcast scalar operands).  A group of GL
+// lanes (2 GL Morton-consecutive targets) shares one stackless traversal; the
+// record load, the traversal control and the vote are shared by the group.
+//
+// Per target and record visit the MAC costs 7 ALU-pipe instructions (the loop
+// is ALU-pipe bound): act = c >= res (ISETP), acc = act & d2 >
+// T_acc, ge = act & d2 >= T_rej (2 FSETP), cnt += acc, f = acc ? f : 0,
+// res = ge ? (acc ? skip : dropw) : res (2 SEL).  The record's fourth word is
+// its drop word (BH_DROP | c, so the inconclusive case needs no per-visit OR);
+// a target opens c iff its updated res <= c (accept and drop move res past c,
+// inactive targets are past it already), so the group vote is one min per
+// lane.  The sentinel record Wn (T_acc = +inf, T_rej = -inf, skip = Wn, drop
+// word Wn + 1) parks finished groups: its targets go inactive without a drop
+// and nobody opens it, so the cursor never passes Wn and needs no clamp.
 #include "walk_common.cuh"
 
 namespace bh {
 
-// ---------------------------------------------------------------- k_walk2
-// The production walk: the same per-lane semantics and the same fp32 operation
-// sequence per target as k_walk (bitwise-identical results), but every lane
-// carries TWO targets and does their arithmetic with Blackwell's packed fp32
-// instructions (FADD2 / FMUL2 / FFMA2: one issue slot, two fp32 results; the
-// node's fields enter as broadcast scalar operands).  The record loads, the
-// traversal control and the vote are shared by the pair, so the issue slots per
-// target-visit drop by ~1/3.  A group of GL lanes (2 GL targets, Morton-
-// consecutive) shares one traversal.
-#ifndef BH_WALK2_BLOCK
-#define BH_WALK2_BLOCK 128
+#ifndef BH_WALK_BLOCK
+#define BH_WALK_BLOCK 128
 #endif
-#ifndef BH_WALK2_UNROLL_SMALL
-#define BH_WALK2_UNROLL_SMALL 3  // visits per loop trip for groups of <= 2 lanes (3 vs 2: cfg5 -2.2%, cfg3 -1.2%, cfg2 -1.4%)
+#ifndef BH_WALK_MINB
+#define BH_WALK_MINB 9  // blocks of 128 threads per SM: 56 registers (36 warps; 10 spills in the loop)
 #endif
-#ifndef BH_WALK2_MINB
-#define BH_WALK2_MINB 5
+#ifndef BH_WALK_UNROLL
+#define BH_WALK_UNROLL 2  // record visits per loop trip, groups of >= 4 lanes
 #endif
-// NP pairs of targets per lane (2 NP targets), GL lanes per group: a group of
-// 2 NP GL Morton-consecutive targets shares one traversal.
-template <int GL, int NP, bool CONT, bool QUAD>
-__global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 && !QUAD ? BH_WALK2_MINB : 4) * 256 / BH_WALK2_BLOCK) k_walk2(const WalkParams P) {
-  constexpr int TPL = 2 * NP;  // targets per lane
+#ifndef BH_WALK_UNROLL_SMALL
+#define BH_WALK_UNROLL_SMALL 3  // groups of <= 2 lanes (3 vs 2: cfg5 -2.2%, cfg3 -1.2%, cfg2 -1.4%, r1)
+#endif
+// Accumulation: every target's contributions are summed in fp32 over blocks
+// of BH_FOLD_TRIPS loop trips of its group's walk, and each block is folded
+// into an outer sum (BH_FOLD = 1: fp32, 2: fp64, 0: one fp32 sum).  The trip
+// counter is uniform over the warp (a non-divergent branch), and the blocks --
+// hence the rounding -- depend only on the group's own walk (the same at any
+// rank count: world > 1 walks the P = 1 groups).  Measured on all 2^24 cfg4
+// targets (profiles/r2_accuracy.md): max relative error 1.26e-4 with one fp32
+// sum, 1.45e-5 with BH_FOLD 1, 6.5e-6 with BH_FOLD 2 (+6% / +15% walk time).
+#ifndef BH_FOLD
+#define BH_FOLD 1
+#endif
+#ifndef BH_OPN_MIN
+#define BH_OPN_MIN 1
+#endif
+#ifndef BH_FOLD_TRIPS
+#define BH_FOLD_TRIPS 16
+#endif
+#if BH_FOLD == 2
+typedef double FoldT;
+#else
+typedef float FoldT;
+#endif
+
+// One target's MAC at record cc (see the header comment); with QUAD the
+// quadrupole factors of a target that does not accept are zeroed too.
+template <bool QUAD>
+__device__ __forceinline__ void mac_one(uint32_t cc, float d2, float tacc, float trej, uint32_t skip, uint32_t dropw,
+                                        uint32_t &res, uint32_t &cnt, float &f, float &g1, float &g2) {
+  if (QUAD) {
+    asm("{\n\t.reg .pred pa, pc, pq;\n\t"
+        "setp.ge.u32 pa, %5, %0;\n\t"
+        "setp.gt.and.f32 pc, %6, %7, pa;\n\t"
+        "setp.ge.and.f32 pq, %6, %8, pa;\n\t"
+        "@pc add.u32 %1, %1, 1;\n\t"
+        "@pq selp.b32 %0, %9, %10, pc;\n\t"
+        "@!pc mov.b32 %2, 0f00000000;\n\t"
+        "@!pc mov.b32 %3, 0f00000000;\n\t"
+        "@!pc mov.b32 %4, 0f00000000;\n\t}"
+        : "+r"(res), "+r"(cnt), "+f"(f), "+f"(g1), "+f"(g2)
+        : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
+  } else {
+    asm("{\n\t.reg .pred pa, pc, pq;\n\t"
+        "setp.ge.u32 pa, %3, %0;\n\t"
+        "setp.gt.and.f32 pc, %4, %5, pa;\n\t"
+        "setp.ge.and.f32 pq, %4, %6, pa;\n\t"
+        "@pc add.u32 %1, %1, 1;\n\t"
+        "@pq selp.b32 %0, %7, %8, pc;\n\t"
+        "@!pc mov.b32 %2, 0f00000000;\n\t}"
+        : "+r"(res), "+r"(cnt), "+f"(f)
+        : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
+  }
+}
+
+// STATS: also count the opened MAC tests (the flop model of bench.py).
+template <int GL, bool CONT, bool QUAD, bool STATS>
+__global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : BH_WALK_MINB) k_walk(const WalkParams P) {
+  constexpr int TPL = 2;                   // targets per lane (one packed pair)
+  constexpr int GT = GL * TPL;             // targets per group
+  constexpr int GPB = BH_WALK_BLOCK / GL;  // groups per block
   const uint32_t full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
   if (P.st->err & ERR_NODE_OVERFLOW) return;
   const uint32_t Wn = P.st->n_records;
-  const uint32_t chunk = blockIdx.x;
-  // Group order.  The block's 256 / GL groups are dealt to its warps in
-  // descending order of their predicted cost (union-walk trips in the last
-  // walk, kept per particle in gcost):
-  // a warp runs until its slowest group is done, so warps of similar groups
-  // idle less (the groups themselves -- which targets walk together -- do not
-  // change, hence neither do the results).  Without costs: Morton order.
-  constexpr int GPB = BH_WALK2_BLOCK / GL;  // groups per block
+  const int lane = threadIdx.x & 31;
+  const uint32_t gmask = GL == 32 ? full : (((1u << GL) - 1u) << (lane & ~(GL - 1)));
+  const int64_t ngroups = P.group_list ? (int64_t)*P.n_groups_dev : (P.n_targets + GT - 1) / GT;
+  const int64_t g0 = (int64_t)blockIdx.x * GPB;
+  if (g0 >= ngroups) return;  // (world > 1: the grid is sized for the most groups a rank can hold)
+  // Group order.  The block's groups are dealt to its warps in descending
+  // order of their predicted cost (the loop trips of the group's last walk,
+  // kept per particle in gcost so that it follows the particles as groups
+  // re-form every step; a group's cost = the larger of its first and last
+  // targets'): a warp runs until its slowest group is done, so warps of
+  // similar groups idle less.  Which targets walk together does not change,
+  // hence neither do the results.  Without costs: Morton order.
   const int gi = lane / GL, gl = lane % GL;
-  int lg = (threadIdx.x >> 5) * (32 / GL) + gi;  // local group of this lane
+  int lg = (threadIdx.x >> 5) * (32 / GL) + gi;
   if (P.gcost) {
     __shared__ uint32_t s_cost[GPB], s_perm[GPB];
-    const int64_t g0 = (int64_t)chunk * GPB;
-    const int64_t ngroups = (P.n_targets + GL * TPL - 1) / (GL * TPL);
     if (threadIdx.x < GPB) {
-      // a group's predicted cost: the last-walk cost recorded on its first and
-      // last targets (costs travel with the particles, groups are re-formed
-      // from the current Morton order every step)
       uint32_t cst = 0u;
       const int64_t g = g0 + threadIdx.x;
       if (g < ngroups) {
-        const int64_t t0 = g * (GL * TPL);
-        const int64_t t1 = min(t0 + GL * TPL, P.n_targets) - 1;
-        const uint32_t p0 = P.use_targets ? P.targets[t0] : (uint32_t)t0;
-        const uint32_t p1 = P.use_targets ? P.targets[t1] : (uint32_t)t1;
-        cst = max(P.gcost[P.vals[p0]], P.gcost[P.vals[p1]]);
+        const int64_t t0 = (P.group_list ? (int64_t)P.group_list[g] : g) * GT;
+        const int64_t t1 = min(t0 + GT, P.n_targets) - 1;
+        cst = max(P.gcost[P.vals[t0]], P.gcost[P.vals[t1]]);
       }
       s_cost[threadIdx.x] = cst;
     }
@@ -75,67 +134,61 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 && !QUAD ? BH_WALK2_M
     __syncthreads();
     lg = (int)s_perm[lg];
   }
-  const int64_t gidx = (int64_t)chunk * GPB + lg;  // global group index
-  const int64_t tbase = gidx * (GL * TPL) + gl;
+  const int64_t gidx = g0 + lg;
+  const bool gin = gidx < ngroups;
+  const int64_t grp = gin ? (P.group_list ? (int64_t)P.group_list[gidx] : gidx) : 0;
+  const int64_t tbase = grp * GT + gl;
   Target T[TPL];
-  bool v[TPL];
+  bool v[TPL], own[TPL];
   bool anyv = false;
 #pragma unroll
   for (int k = 0; k < TPL; k++) {
     const int64_t t = tbase + (int64_t)k * GL;
-    v[k] = t < P.n_targets;
+    v[k] = gin && t < P.n_targets;
     anyv |= v[k];
     if (v[k]) T[k] = load_target(P, t);
     else { T[k].p = 0; T[k].Li = 0; T[k].s = 0; T[k].me = make_float4(0.f, 0.f, 0.f, 0.f); }
+    own[k] = v[k] && (!P.own_check || (T[k].s >= P.own_lo && T[k].s < P.own_hi));
   }
-  uint32_t Li[TPL], res[TPL], cnt[TPL];
+  uint32_t res[TPL], cnt[TPL], nop[TPL];
   float ax[TPL], ay[TPL], az[TPL];
-  F2 X[NP], Y[NP], Z[NP];
 #pragma unroll
   for (int k = 0; k < TPL; k++) {
-    Li[k] = T[k].Li;
     res[k] = v[k] ? 0u : 0xffffffffu;
     cnt[k] = 0;
+    nop[k] = 0;
     ax[k] = ay[k] = az[k] = 0.f;
   }
-#pragma unroll
-  for (int j = 0; j < NP; j++) {
-    X[j] = pk2(T[2 * j].me.x, T[2 * j + 1].me.x);
-    Y[j] = pk2(T[2 * j].me.y, T[2 * j + 1].me.y);
-    Z[j] = pk2(T[2 * j].me.z, T[2 * j + 1].me.z);
-  }
+  const F2 X = pk2(T[0].me.x, T[1].me.x), Y = pk2(T[0].me.y, T[1].me.y), Z = pk2(T[0].me.z, T[1].me.z);
+  const uint32_t LiA = T[0].Li, LiB = T[1].Li;
   const F2 E2 = pk2(P.eps2, P.eps2);
   const bool gvalid = (__ballot_sync(full, anyv) & gmask) != 0u;
   const Rec *__restrict__ rec = P.rec;
-  asm volatile("" : "+l"(rec));  // base in a register (no per-iteration constant reload)
   uint32_t gmask2 = gmask;
   asm volatile("" : "+r"(gmask2));  // a plain register: the group test is one LOP3
   uint32_t c = gvalid ? 0u : Wn;
-  uint32_t git = 0;  // union-walk trips (2 visits) of this lane's group (its cost)
-  // a finished group parks on the sentinel record Wn (T_acc = T_rej = +inf,
-  // skip = Wn: nothing is accepted or queued there) until the warp is done
-  // two visits per trip: the exit vote and the cost counter run once per trip
-  // (a parked group stays on the sentinel, so the extra visit is harmless)
+  uint32_t git = 0;  // live loop trips of this lane's group (its cost; visits per trip = the unroll)
+#if BH_FOLD
+  FoldT ox[TPL], oy[TPL], oz[TPL];
+#pragma unroll
+  for (int k = 0; k < TPL; k++) ox[k] = oy[k] = oz[k] = (FoldT)0;
+  uint32_t trip = 0;
+#endif
   if (__any_sync(full, c < Wn)) for (;;) {
 #pragma unroll
-   for (int u = 0; u < (GL <= 2 ? BH_WALK2_UNROLL_SMALL : BH_WALK2_UNROLL); u++) {
-    const uint32_t cc = c;
-    float4 cm;
-    uint4 au;
-    ld_rec(rec + cc, cm, au);
-    const uint32_t skip = au.z;
-    const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
-    uint32_t opn = 0u;
-#pragma unroll
-    for (int j = 0; j < NP; j++) {
-      const int a = 2 * j, b = 2 * j + 1;
-      const F2 DX = sub2(pk2(cm.x, cm.x), X[j]), DY = sub2(pk2(cm.y, cm.y), Y[j]),
-               DZ = sub2(pk2(cm.z, cm.z), Z[j]);
+    for (int u = 0; u < (GL <= 2 ? BH_WALK_UNROLL_SMALL : BH_WALK_UNROLL); u++) {
+      const uint32_t cc = c;
+      float4 cm;
+      uint4 au;
+      ld_rec(rec + cc, cm, au);
+      const uint32_t skip = au.z, dropw = au.w;
+      const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
+      const F2 DX = sub2(pk2(cm.x, cm.x), X), DY = sub2(pk2(cm.y, cm.y), Y), DZ = sub2(pk2(cm.z, cm.z), Z);
       const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
       float d2A, d2B;
       up2(D2, d2A, d2B);
-      // interaction for both targets of the pair, branch-free (f zeroed below
-      // for a target that does not accept the record)
+      // the interaction of both targets, branch-free (f zeroed for a target
+      // that does not accept the record)
       float r2A, r2B;
       up2(add2(D2, E2), r2A, r2B);
       const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
@@ -158,81 +211,157 @@ __global__ void __launch_bounds__(BH_WALK2_BLOCK, (NP == 1 && !QUAD ? BH_WALK2_M
         up2(INV5, g1A, g1B);
         up2(mul2(mul2(pk2(-2.5f, -2.5f), SQ), INV7), g2A, g2B);
       }
-      // per-target MAC (identical decisions to k_walk); an inconclusive fp32
-      // test drops the target out (resume = BH_DROP | c): k_walk_resume continues it
-      // (a record containing the target is opened, never accepted: NaN distance)
+      // per-target MAC; a record containing the target is opened, never
+      // accepted (CONT: NaN distance)
       float qA = d2A, qB = d2B;
       if (CONT) {
-        const bool cA = (cc <= Li[a]) & (skip > Li[a]), cB = (cc <= Li[b]) & (skip > Li[b]);
+        const bool cA = (cc <= LiA) & (skip > LiA), cB = (cc <= LiB) & (skip > LiB);
         const float qnan = __int_as_float(0x7fffffff);
         qA = cA ? qnan : d2A;
         qB = cB ? qnan : d2B;
       }
-      if (QUAD) {
-        mac_pair_q(cc, qA, qB, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA, fB, g1A, g1B, g2A, g2B);
-      } else {
-        mac_pair(cc, qA, qB, tacc, trej, skip, res[a], res[b], cnt[a], cnt[b], opn, fA, fB);
-      }
+#if !BH_OPN_MIN
+      // (variant: the open test from the pre-update state, off the SEL chain)
+      uint32_t opn_pred;
+      asm("{\n\t.reg .pred pa, pb, po;\n\t"
+          "setp.ge.u32 pa, %1, %2;\n\t"
+          "setp.ge.u32 pb, %1, %3;\n\t"
+          "setp.ltu.and.f32 pa, %4, %6, pa;\n\t"
+          "setp.ltu.and.f32 pb, %5, %6, pb;\n\t"
+          "or.pred po, pa, pb;\n\t"
+          "selp.u32 %0, 1, 0, po;\n\t}"
+          : "=r"(opn_pred) : "r"(cc), "r"(res[0]), "r"(res[1]), "f"(qA), "f"(qB), "f"(trej));
+#endif
+      mac_one<QUAD>(cc, qA, tacc, trej, skip, dropw, res[0], cnt[0], fA, g1A, g2A);
+      mac_one<QUAD>(cc, qB, tacc, trej, skip, dropw, res[1], cnt[1], fB, g1B, g2B);
       const F2 FF = pk2(fA, fB);
       // packed accumulate on (a, b) register pairs (this form avoids ptxas moves)
       asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
-          : "+f"(ax[a]), "+f"(ax[b]) : "l"(FF.v), "l"(DX.v));
+          : "+f"(ax[0]), "+f"(ax[1]) : "l"(FF.v), "l"(DX.v));
       asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
-          : "+f"(ay[a]), "+f"(ay[b]) : "l"(FF.v), "l"(DY.v));
+          : "+f"(ay[0]), "+f"(ay[1]) : "l"(FF.v), "l"(DY.v));
       asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
-          : "+f"(az[a]), "+f"(az[b]) : "l"(FF.v), "l"(DZ.v));
+          : "+f"(az[0]), "+f"(az[1]) : "l"(FF.v), "l"(DZ.v));
       if (QUAD) {
         const F2 G1 = pk2(g1A, g1B), G2 = pk2(g2A, g2B);
-        F2 AX = pk2(ax[a], ax[b]), AY = pk2(ay[a], ay[b]), AZ = pk2(az[a], az[b]);
+        F2 AX = pk2(ax[0], ax[1]), AY = pk2(ay[0], ay[1]), AZ = pk2(az[0], az[1]);
         AX = fma2(G2, DX, fma2(G1, QX, AX));
         AY = fma2(G2, DY, fma2(G1, QY, AY));
         AZ = fma2(G2, DZ, fma2(G1, QZ, AZ));
-        up2(AX, ax[a], ax[b]);
-        up2(AY, ay[a], ay[b]);
-        up2(AZ, az[a], az[b]);
+        up2(AX, ax[0], ax[1]);
+        up2(AY, ay[0], ay[1]);
+        up2(AZ, az[0], az[1]);
+      }
+      // a target opened cc iff it was active and its res stayed <= cc
+      if (STATS) {
+        nop[0] += res[0] <= cc ? 1u : 0u;
+        nop[1] += res[1] <= cc ? 1u : 0u;
+      }
+#if BH_OPN_MIN
+      const bool opn = min(res[0], res[1]) <= cc;
+#else
+      const bool opn = opn_pred != 0u;
+#endif
+      if (GL == 32) {
+        c = __any_sync(full, opn) ? cc + 1u : skip;
+      } else {
+        c = (__ballot_sync(full, opn) & gmask2) ? cc + 1u : skip;
       }
     }
-    if (GL == 32) {
-      c = min(__any_sync(full, opn != 0u) ? cc + 1u : skip, Wn);
-    } else {
-      const uint32_t nxt = (__ballot_sync(full, opn != 0u) & gmask2) ? cc + 1u : skip;
-      c = min(nxt, Wn);
-    }
-   }
     const bool live = c < Wn;
     git += live ? 1u : 0u;
+#if BH_FOLD
+    if (++trip == BH_FOLD_TRIPS) {  // warp-uniform
+      trip = 0;
+#pragma unroll
+      for (int k = 0; k < TPL; k++) {
+        ox[k] += (FoldT)ax[k];
+        oy[k] += (FoldT)ay[k];
+        oz[k] += (FoldT)az[k];
+        ax[k] = ay[k] = az[k] = 0.f;
+      }
+    }
+#endif
     if (!__any_sync(full, live)) break;
+  }
+  double dax[TPL], day[TPL], daz[TPL];
+#pragma unroll
+  for (int k = 0; k < TPL; k++) {
+#if BH_FOLD
+    dax[k] = (double)ox[k] + (double)ax[k];
+    day[k] = (double)oy[k] + (double)ay[k];
+    daz[k] = (double)oz[k] + (double)az[k];
+#else
+    dax[k] = (double)ax[k];
+    day[k] = (double)ay[k];
+    daz[k] = (double)az[k];
+#endif
   }
   if (P.gcost) {
 #pragma unroll
     for (int k = 0; k < TPL; k++)
       if (v[k]) P.gcost[T[k].s] = git;  // this walk's cost of the target's group
   }
-  unsigned long long wc = 0;
+  unsigned long long wc = 0, wo = 0;
   bool redo[TPL];
 #pragma unroll
   for (int k = 0; k < TPL; k++) {
-    redo[k] = v[k] && res[k] >= BH_DROP;
-    if (!CONT && !redo[k]) cnt[k] -= v[k] ? 1u : 0u;  // own record: "accepted", zero contribution
-    wc += redo[k] ? 0u : cnt[k];
+    redo[k] = own[k] && res[k] >= BH_DROP;
+    if (!CONT && v[k] && res[k] < BH_DROP) cnt[k] -= 1u;  // own record: "accepted", zero contribution
+    wc += (own[k] && !redo[k]) ? cnt[k] : 0u;
+    if (STATS) wo += own[k] ? nop[k] : 0u;
   }
-  for (int o = 16; o; o >>= 1) wc += __shfl_xor_sync(full, wc, o);
+  for (int o = 16; o; o >>= 1) {
+    wc += __shfl_xor_sync(full, wc, o);
+    if (STATS) wo += __shfl_xor_sync(full, wo, o);
+  }
   if (lane == 0 && wc) {
     atomicAdd(&P.st->interactions, wc);
     atomicAdd(&P.st->interactions_cum, wc);
   }
+  if (STATS && lane == 0 && wo) {
+    atomicAdd(&P.st->opens, wo);
+    atomicAdd(&P.st->opens_cum, wo);
+  }
 #pragma unroll
   for (int k = 0; k < TPL; k++) {
-    if (!v[k]) continue;
+    if (!own[k]) continue;
     if (redo[k])
-      push_resume(P, tbase + (int64_t)k * GL, res[k], ax[k], ay[k], az[k], cnt[k],
-                  (!CONT && Li[k] < (res[k] & ~BH_DROP)) ? 1u : 0u);
-    else finish(P, T[k], (double)ax[k], (double)ay[k], (double)az[k], cnt[k]);
+      push_resume(P, tbase + (int64_t)k * GL, res[k], dax[k], day[k], daz[k], cnt[k],
+                  (!CONT && T[k].Li < (res[k] & ~BH_DROP)) ? 1u : 0u);
+    else finish(P, T[k], dax[k], day[k], daz[k], cnt[k]);
   }
 }
 
+// world > 1: the P = 1 groups (GT consecutive sorted positions) that hold at
+// least one particle of this rank's storage range [lo, hi)
+__global__ void k_own_group_flags(const uint32_t *__restrict__ vals, uint32_t *__restrict__ flag, int64_t n, int gt,
+                                  uint32_t lo, uint32_t hi) {
+  const int64_t ng = (n + gt - 1) / gt;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g < ng) {
+    uint32_t f = 0;
+    const int64_t e = (g + 1) * gt < n ? (g + 1) * gt : n;
+    for (int64_t t = g * gt; t < e; t++) {
+      const uint32_t s = vals[t];
+      f |= (s >= lo && s < hi) ? 1u : 0u;
+    }
+    flag[g] = f;
+  }
+  if (g == ng) flag[ng] = 0;
+}
+__global__ void k_own_group_compact(const uint32_t *__restrict__ pre, uint32_t *__restrict__ list, int64_t ng,
+                                    uint32_t *__restrict__ count) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g < ng && pre[g + 1] != pre[g]) list[pre[g]] = (uint32_t)g;
+  if (g == ng) *count = pre[ng];
+}
+
+// walk_group code -> lanes per group (66: 8, 67: 4, 68: 2)
+int walk_lanes(int group) { return group == 66 ? 8 : group == 68 ? 2 : 4; }
+
 cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
-  if (a.n_targets <= 0) return cudaSuccess;
+  if (a.n <= 0) return cudaSuccess;
   WalkParams P;
   P.rec = W.rec;
   P.quad = a.quad && W.qrec;
@@ -241,7 +370,6 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.rec_item = W.rec_item;
   P.nstart = W.nstart;
   P.vals = W.vals[a.buf];
-  P.targets = W.targets;
   P.uid = W.uid;
   P.st = W.status;
   P.icount = W.icount;
@@ -255,8 +383,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.vel4 = W.vel4;
   P.acc_out = a.acc_out;
   P.user_order = a.user_order;
-  P.n_targets = a.n_targets;
-  P.use_targets = a.use_targets;
+  P.n_targets = a.n;
   P.mode = a.mode;
   P.eps2 = a.eps2;
   P.G = a.G;
@@ -264,40 +391,59 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.dt = a.dt;
   P.theta2 = a.theta2;
   P.own_lo = a.own_lo;
+  P.own_hi = a.own_hi;
+  P.own_check = a.own_check;
   P.num_sms = a.num_sms > 0 ? a.num_sms : 148;
-  if (!a.stats && a.group >= 80 && a.group <= 95) {
-    const cudaError_t e = launch_walk_lane(P, a.group, a.need_cont, a.n_targets, s);
+  const int GL = walk_lanes(a.group), GT = 2 * GL;
+  const int64_t ng_all = (a.n + GT - 1) / GT;
+  int64_t ng_max = ng_all;
+  P.group_list = nullptr;
+  P.n_groups_dev = nullptr;
+  if (a.own_check) {
+    // the list of P = 1 groups with an own particle (in W.targets) and its
+    // length on the device; flags and scan in accu (ng + 1 u32 fit in 3 n floats)
+    uint32_t *flag = (uint32_t *)W.accu;
+    const unsigned gb = (unsigned)((ng_all + 1 + 255) / 256);
+    k_own_group_flags<<<gb, 256, 0, s>>>(P.vals, flag, a.n, GT, a.own_lo, a.own_hi);
+    cudaError_t e = launch_scan_u32(flag, ng_all + 1, W.scan_tmp, s);
     if (e != cudaSuccess) return e;
-  } else if (!a.stats && (a.group == 0 || a.group >= 64)) {
-    // production path (k_walk2): packed fp32, lanes per group x targets per lane
-    //   66 / 67 / 68: 8 / 4 / 2 lanes x 2 targets   (api.cu picks 67 or 68 for 0)
-    //   64: 32 lanes x 2 targets;  65 / 69 / 70: 8 / 4 / 2 lanes x 4 targets
+    uint32_t *cnt = &W.status->n_own_groups;
+    k_own_group_compact<<<gb, 256, 0, s>>>(flag, W.targets, ng_all, cnt);
+    P.group_list = W.targets;
+    P.n_groups_dev = cnt;
+    const int64_t own_n = (int64_t)a.own_hi - a.own_lo;
+    ng_max = own_n < ng_all ? own_n : ng_all;  // every own particle is in one group
+  }
+  if (ng_max > 0) {
+    constexpr int WB = BH_WALK_BLOCK;
+    const unsigned grid = (unsigned)((ng_max + WB / GL - 1) / (WB / GL));
     const bool cont = a.need_cont;
-    constexpr int WB = BH_WALK2_BLOCK;
-    const unsigned grid2 = (unsigned)((a.n_targets + 2 * WB - 1) / (2 * WB));
-    const unsigned g4 = (unsigned)((a.n_targets + 4 * WB - 1) / (4 * WB));
-#define BH_WALK2_LAUNCH(GLv, NPv, gr)                                              \
-  if (P.quad) {                                                                   \
-    if (cont) k_walk2<GLv, NPv, true, true><<<gr, WB, 0, s>>>(P);                \
-    else k_walk2<GLv, NPv, false, true><<<gr, WB, 0, s>>>(P);                    \
-  } else {                                                                        \
-    if (cont) k_walk2<GLv, NPv, true, false><<<gr, WB, 0, s>>>(P);               \
-    else k_walk2<GLv, NPv, false, false><<<gr, WB, 0, s>>>(P);                   \
+#define BH_WALK_LAUNCH(GLv)                                                      \
+  if (a.stats) {                                                                 \
+    if (P.quad) {                                                                \
+      if (cont) k_walk<GLv, true, true, true><<<grid, WB, 0, s>>>(P);            \
+      else k_walk<GLv, false, true, true><<<grid, WB, 0, s>>>(P);                \
+    } else {                                                                     \
+      if (cont) k_walk<GLv, true, false, true><<<grid, WB, 0, s>>>(P);           \
+      else k_walk<GLv, false, false, true><<<grid, WB, 0, s>>>(P);               \
+    }                                                                            \
+  } else {                                                                       \
+    if (P.quad) {                                                                \
+      if (cont) k_walk<GLv, true, true, false><<<grid, WB, 0, s>>>(P);           \
+      else k_walk<GLv, false, true, false><<<grid, WB, 0, s>>>(P);               \
+    } else {                                                                     \
+      if (cont) k_walk<GLv, true, false, false><<<grid, WB, 0, s>>>(P);          \
+      else k_walk<GLv, false, false, false><<<grid, WB, 0, s>>>(P);              \
+    }                                                                            \
   }
-    switch (a.group) {
-      case 64: BH_WALK2_LAUNCH(32, 1, grid2) break;
-      case 65: BH_WALK2_LAUNCH(8, 2, g4) break;
-      case 66: BH_WALK2_LAUNCH(8, 1, grid2) break;
-      case 68: BH_WALK2_LAUNCH(2, 1, grid2) break;
-      case 69: BH_WALK2_LAUNCH(4, 2, g4) break;
-      case 70: BH_WALK2_LAUNCH(2, 2, g4) break;
-      default: BH_WALK2_LAUNCH(4, 1, grid2) break;  // 67
+    switch (GL) {
+      case 8: BH_WALK_LAUNCH(8) break;
+      case 2: BH_WALK_LAUNCH(2) break;
+      default: BH_WALK_LAUNCH(4) break;
     }
-#undef BH_WALK2_LAUNCH
-  } else {
-    launch_walk_simple(P, a.group, a.stats, a.n_targets, s);
+#undef BH_WALK_LAUNCH
   }
-  launch_walk_resume(P, a.n_targets, s);
+  launch_walk_resume(P, a.n, s);
   return cudaGetLastError();
 }
 

@@ -1,8 +1,7 @@
 // walk_common.cuh -- what the K6 walk kernels share: the launch parameters,
 // target load / epilogue (K7 fused leapfrog) / drop-out queue, the quadrupole
-// term, the packed-fp32 (f32x2) helpers and the MAC predicate blocks.
-//   walk.cu          k_walk2 (production) and launch_walk (the dispatcher)
-//   walk_variants.cu k_walk (statistics, group-size variants) and the k_walk_lane family
+// term and the packed-fp32 (f32x2) helpers.
+//   walk.cu          k_walk (production, every group size) and launch_walk
 //   walk_resume.cu   k_walk_resume (continuation of inconclusive MAC tests, fp64)
 //
 // PAPER.md:500-504 (§3): "The most computationally intensive part of the
@@ -13,29 +12,28 @@
 // are always opened (L5), Plummer softening on every source (L6), G applied
 // last (L7); "interactions" = accepted cells + particles j != i (L21).
 //
-// Per-particle semantics with warp-shared traversal.  Targets
-// are taken in Morton order; a group of G lanes (G = 32: a warp) walks ONE
-// stackless DFS over the record array: at record c every active lane evaluates
-// its own MAC; lanes that accept c interact with it and become inactive until
-// skip(c) (their subtree is done); the group descends (c + 1) if any active lane
-// opens c, else jumps to skip(c).  Each lane therefore sees exactly its own
-// Barnes-Hut frontier, in DFS order -- identical decisions to the oracle's
-// recursive walk -- while the group's record loads are one broadcast address.
+// Per-particle semantics with shared traversal.  Targets are
+// taken in Morton order; a group of GL lanes (2 GL targets) walks ONE
+// stackless DFS over the record array: at record c every active target
+// evaluates its own MAC; targets that accept c interact with it and become
+// inactive until skip(c) (their subtree is done); the group descends (c + 1) if
+// any active target opens c, else jumps to skip(c).  Each target therefore
+// sees exactly its own Barnes-Hut frontier, in DFS order -- identical
+// decisions to the oracle's recursive walk -- while the group's record loads
+// are one broadcast address.
 //
 // MAC decisions are exact.  The fast kernel decides with the fp32 thresholds
 // T_acc / T_rej of com.cu (d2_32 > T_acc: accept for sure; d2_32 < T_rej: open
-// for sure).  A lane whose d2_32 falls between them (~1e-6 of the tests) drops
-// out of the fast walk at that record and is queued with its partial sums;
-// k_walk_resume then continues each such target's DFS from that record alone,
-// with the oracle's fp64 test on the ambiguous nodes.  The fast loop thus
-// carries no fp64 code and no divergent branch.
+// for sure).  A target whose d2_32 falls between them (~1e-6 of the tests)
+// drops out of the fast walk at that record and is queued with its partial
+// sums; k_walk_resume then continues each such target's DFS from that record
+// alone, with the oracle's fp64 test on the ambiguous nodes.
 //
 // Interaction (fp32): r2 = d2 + eps^2, f = M rsqrt(r2)^3, a += f (dx, dy, dz):
-// 18 flops + 1 MUFU.RSQ, summed sequentially in fp32 in the lane's own DFS
-// order (so the result does not depend on the group size or the rank count).
-// Measured max per-particle error vs the fp64 oracle: <= 2.5e-5 on cfg1-cfg4
-// (DESIGN.md §6); -DBH_FOLD64 folds the fp32 partials into fp64 every 64
-// interactions (max error <= 1.8e-5 -> 2.7e-6 on cfg2, 17% slower walk).
+// 18 flops + 1 MUFU.RSQ, in the target's own DFS order; the fp32 sums run over
+// blocks of BH_FOLD_TRIPS loop trips of the group's walk and are folded into
+// an outer sum (walk.cu; measured max error over all 2^24 cfg4 targets 1.3e-4
+// with one fp32 sum, 1.5e-5 with the fold).
 //
 // K7 (mode 1): v += a * kick (kick = dt/2 on the first step, dt after; reading
 // L8), x += v dt, written in place to pos4 / vel4 of the particle's storage slot
@@ -57,7 +55,6 @@ struct WalkParams {
   const uint32_t *__restrict__ rec_item;  // record -> level item
   const uint32_t *__restrict__ nstart;
   const uint32_t *__restrict__ vals;
-  const uint32_t *__restrict__ targets;
   const uint32_t *__restrict__ uid;
   DevStatus *st;
   uint32_t *icount;
@@ -69,14 +66,20 @@ struct WalkParams {
   float4 *pos4;
   float4 *vel4;
   float *acc_out;  // mode 0: acc_out[3 uid[s]] (user_order) or acc_out[3 (s - own_lo)]
-  uint32_t *gcost;  // k_walk2: per storage id, the last-walk trips of its group (or null)
+  uint32_t *gcost;  // group-order cost per storage id: the loop trips of its group's last walk (or null)
   int user_order;
-  int64_t n_targets;
-  int use_targets;
+  int64_t n_targets;   // all particles (targets are sorted positions 0 .. n-1)
+  // world > 1: the walk runs the P = 1 groups (GT consecutive sorted
+  // positions) that hold at least one own particle -- group_list[0 ..
+  // *n_groups_dev) -- and writes only the own targets' results, so every
+  // target is summed in the same group, hence the same blocks, as at P = 1
+  const uint32_t *group_list;
+  const uint32_t *n_groups_dev;
+  int own_check;
   int mode;
   float eps2, G, kick, dt;
   double theta2;
-  uint32_t own_lo;
+  uint32_t own_lo, own_hi;
   int num_sms;
 };
 
@@ -123,7 +126,7 @@ struct Target {
 
 __device__ __forceinline__ Target load_target(const WalkParams &P, int64_t t) {
   Target T;
-  T.p = P.use_targets ? P.targets[t] : (uint32_t)t;
+  T.p = (uint32_t)t;  // a sorted position
   T.Li = P.nstart[T.p + 1] - 1u;  // the particle's own record
   T.me = P.rec[T.Li].cm;
   T.s = P.vals[T.p];
@@ -160,8 +163,8 @@ __device__ __forceinline__ void finish(const WalkParams &P, const Target &T, dou
 // cdrop with the oracle's exact test.  `own` = 1 if the count includes the
 // target's own record (the CONT = false kernels accept it with a zero
 // contribution; the resume kernel opens it, as the oracle does).
-__device__ __forceinline__ void push_resume(const WalkParams &P, int64_t t, uint32_t res, float ax, float ay, float az,
-                                            uint32_t cnt, uint32_t own) {
+__device__ __forceinline__ void push_resume(const WalkParams &P, int64_t t, uint32_t res, double ax, double ay,
+                                            double az, uint32_t cnt, uint32_t own) {
   const unsigned long long k = atomicAdd(&P.st->n_redo, 1ull);
   P.redo[k] = (uint32_t)t;
   if ((int64_t)k < P.cap_resume) {
@@ -171,15 +174,13 @@ __device__ __forceinline__ void push_resume(const WalkParams &P, int64_t t, uint
     r.az = az;
     r.cnt = cnt - own;
     r.cdrop = res & ~BH_DROP;
-    r.pad[0] = r.pad[1] = r.pad[2] = 0u;
     P.resume[k] = r;
   }
 }
 
 // ---------------------------------------------------------------- packed fp32
 // Blackwell's packed fp32 instructions (FADD2 / FMUL2 / FFMA2: one issue slot,
-// two fp32 results), used by k_walk2 and k_walk_lane to carry two targets per
-// lane.
+// two fp32 results), used by k_walk to carry two targets per lane.
 struct F2 {
   unsigned long long v;
 };
@@ -221,79 +222,6 @@ __device__ __forceinline__ void ld_rec(const Rec *p, float4 &cm, uint4 &au) {
                : "l"(p));
 }
 
-// One target's MAC decision at record cc, as bit masks (few live predicates):
-//   act = cc >= res (and, with CONT, the record does not contain the target)
-//   acc = act & d2 > T_acc      -> interact (f kept), cnt += 1, res = skip
-//   amb = act & !acc & d2 >= T_rej -> inconclusive: res = BH_DROP | cc (the
-//                                   target drops out; k_walk_resume continues it)
-//   opn |= act & d2 < T_rej     -> the lane descends
-// Identical decisions to k_walk / k_walk2.
-__device__ __forceinline__ void mac_pair(uint32_t cc, float d2A, float d2B, float tacc, float trej, uint32_t skip,
-                                         uint32_t &resA, uint32_t &resB, uint32_t &cntA, uint32_t &cntB,
-                                         uint32_t &opn, float &fA, float &fB) {
-  const uint32_t drop = BH_DROP | cc;
-  asm("{\n\t.reg .pred pa, pc, pq, pb, pd, pr, po;\n\t"
-      "setp.ge.u32 pa, %9, %0;\n\t"                 // act A
-      "setp.gt.and.f32 pc, %10, %12, pa;\n\t"       // acc A
-      "setp.ge.and.f32 pq, %10, %13, pa;\n\t"       // acc-or-amb A
-      "setp.ge.u32 pb, %9, %1;\n\t"                 // act B
-      "setp.gt.and.f32 pd, %11, %12, pb;\n\t"       // acc B
-      "setp.ge.and.f32 pr, %11, %13, pb;\n\t"       // acc-or-amb B
-      "@pc add.u32 %2, %2, 1;\n\t"
-      "@pd add.u32 %3, %3, 1;\n\t"
-      "@pq selp.b32 %0, %14, %15, pc;\n\t"   // acc: skip; amb: BH_DROP | cc (dropped out)
-      "@pr selp.b32 %1, %14, %15, pd;\n\t"
-      "@!pc mov.b32 %5, 0f00000000;\n\t"
-      "@!pd mov.b32 %6, 0f00000000;\n\t"
-      "not.pred pq, pq;\n\t"
-      "not.pred pr, pr;\n\t"
-      "and.pred pa, pa, pq;\n\t"
-      "and.pred pb, pb, pr;\n\t"
-      "or.pred po, pa, pb;\n\t"
-      "@po mov.b32 %4, 1;\n\t}"
-      : "+r"(resA), "+r"(resB), "+r"(cntA), "+r"(cntB), "+r"(opn), "+f"(fA), "+f"(fB)
-      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip), "r"(drop));
-}
-
-// mac_pair that also zeroes the quadrupole factors (g1, g2) of targets that do
-// not accept the record
-__device__ __forceinline__ void mac_pair_q(uint32_t cc, float d2A, float d2B, float tacc, float trej, uint32_t skip,
-                                           uint32_t &resA, uint32_t &resB, uint32_t &cntA, uint32_t &cntB,
-                                           uint32_t &opn, float &fA, float &fB, float &g1A, float &g1B, float &g2A,
-                                           float &g2B) {
-  const uint32_t drop = BH_DROP | cc;
-  asm("{\n\t.reg .pred pa, pc, pq, pb, pd, pr, po;\n\t"
-      "setp.ge.u32 pa, %13, %0;\n\t"
-      "setp.gt.and.f32 pc, %14, %16, pa;\n\t"
-      "setp.ge.and.f32 pq, %14, %17, pa;\n\t"
-      "setp.ge.u32 pb, %13, %1;\n\t"
-      "setp.gt.and.f32 pd, %15, %16, pb;\n\t"
-      "setp.ge.and.f32 pr, %15, %17, pb;\n\t"
-      "@pc add.u32 %2, %2, 1;\n\t"
-      "@pd add.u32 %3, %3, 1;\n\t"
-      "@pq selp.b32 %0, %18, %19, pc;\n\t"
-      "@pr selp.b32 %1, %18, %19, pd;\n\t"
-      "@!pc mov.b32 %5, 0f00000000;\n\t"
-      "@!pd mov.b32 %6, 0f00000000;\n\t"
-      "@!pc mov.b32 %7, 0f00000000;\n\t"
-      "@!pd mov.b32 %8, 0f00000000;\n\t"
-      "@!pc mov.b32 %9, 0f00000000;\n\t"
-      "@!pd mov.b32 %10, 0f00000000;\n\t"
-      "not.pred pq, pq;\n\t"
-      "not.pred pr, pr;\n\t"
-      "and.pred pa, pa, pq;\n\t"
-      "and.pred pb, pb, pr;\n\t"
-      "or.pred po, pa, pb;\n\t"
-      "@po mov.b32 %4, 1;\n\t}"
-      : "+r"(resA), "+r"(resB), "+r"(cntA), "+r"(cntB), "+r"(opn), "+f"(fA), "+f"(fB), "+f"(g1A), "+f"(g1B),
-        "+f"(g2A), "+f"(g2B)
-      : "r"(cc), "r"(cc), "r"(cc), "f"(d2A), "f"(d2B), "f"(tacc), "f"(trej), "r"(skip), "r"(drop));
-}
-
-#ifndef BH_WALK2_UNROLL
-#define BH_WALK2_UNROLL 2
-#endif
-
 // k_walk_resume geometry (walk_resume.cu; launch_walk clamps the stack-depth
 // test hook to RESUME_STACK)
 constexpr int RESUME_WARPS = 4;
@@ -305,9 +233,16 @@ constexpr int RESUME_WARPS = 4;
 #endif
 constexpr int RESUME_STACK = BH_RESUME_STACK_N;
 
-// launchers of the kernels outside walk.cu (all take launch_walk's parameters)
-void launch_walk_simple(const WalkParams &P, int group, bool stats, int64_t n_targets, cudaStream_t s);
-cudaError_t launch_walk_lane(const WalkParams &P, int group, bool cont, int64_t n_targets, cudaStream_t s);
 void launch_walk_resume(const WalkParams &P, int64_t n_targets, cudaStream_t s);
+
+// level of record c: its level-ordered item's level (levels 0 .. 22, 22 =
+// bucket member), from the level offsets of K4
+__device__ __forceinline__ uint32_t record_level(const WalkParams &P, uint32_t c) {
+  const uint32_t it = P.rec_item[c];
+  uint32_t l = 0;
+#pragma unroll 1
+  while (l + 1 < BH_NLEVELS && P.st->lvl_offset[l + 1] <= it) l++;
+  return l;
+}
 
 }  // namespace bh

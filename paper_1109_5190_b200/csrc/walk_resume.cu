@@ -48,7 +48,7 @@ __device__ __forceinline__ bool resume_visit(const WalkParams &P, const Target &
   const bool cont = (c <= T.Li) & (au.z > T.Li);
   bool acc = !cont & (d2 > __uint_as_float(au.x));
   if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
-    acc = exact_accept(P.lvl_mom, P.rec_item, c, au.w & META_LEVEL_MASK, T.me.x, T.me.y, T.me.z, Ld, P.theta2);
+    acc = exact_accept(P.lvl_mom, P.rec_item, c, record_level(P, c), T.me.x, T.me.y, T.me.z, Ld, P.theta2);
     A.fb++;
   }
   if (acc) {
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(32 * RESUME_WARPS, BH_RESUME_MINB) k_walk_resu
   for (unsigned long long k = blockIdx.x * (unsigned long long)RESUME_WARPS + w; k < nredo;
        k += (unsigned long long)gridDim.x * RESUME_WARPS) {
     const Target T = load_target(P, P.redo[k]);
-    float pax = 0.f, pay = 0.f, paz = 0.f;
+    double pax = 0.0, pay = 0.0, paz = 0.0;
     uint32_t pcnt = 0, c0 = 0;
     if ((int64_t)k < P.cap_resume) {
       const ResumeState r = P.resume[k];
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(32 * RESUME_WARPS, BH_RESUME_MINB) k_walk_resu
       atomicAdd(&P.st->fallbacks, (unsigned long long)A.fb);
       atomicAdd(&P.st->opens, (unsigned long long)A.nop);
       atomicAdd(&P.st->opens_cum, (unsigned long long)A.nop);
-      finish(P, T, (double)pax + A.ax, (double)pay + A.ay, (double)paz + A.az, cnt);
+      finish(P, T, pax + A.ax, pay + A.ay, paz + A.az, cnt);
     }
     __syncwarp();
   }

@@ -260,11 +260,13 @@ def test_errors(BH):
     assert e.value.code == -3
 
 
-@pytest.mark.parametrize("cfg,group", [("cfg2", g) for g in (1, 4, 16, 32, 64, 65, 66, 67, 68, 69, 70, 80, 81, 82, 83, 84, 85, 92, 93, 94)]
-                         + [("cfg3", g) for g in (1, 32, 67, 80, 81, 82, 83, 84, 85, 90, 92, 93, 94, 95)])
-def test_walk_group_invariance(BH, cfg, group):
-    """The traversal-sharing group size changes nothing: bitwise equal forces
-    (cfg2: theta = 0.5, containment test elided; cfg3: theta = 0.7, kept)."""
+@pytest.mark.parametrize("cfg,group", [(c, g) for c in ("cfg2", "cfg3") for g in (66, 67, 68)])
+def test_walk_group_sizes(BH, cfg, group):
+    """The traversal-sharing group size (8 / 4 / 2 lanes) never changes a MAC
+    decision: interaction counts integer-equal to the oracle's; a target's fp32
+    block sums follow its group's walk, so forces agree to rounding (and with
+    the oracle within 1e-4).  cfg2: theta = 0.5 (containment test elided);
+    cfg3: theta = 0.7 (containment folded into the thresholds)."""
     m, p, v = bhgen.generate(cfg, n=20000)
     prm = bhgen.params(cfg)
     a = BH(m, p, v, **prm)
@@ -273,12 +275,16 @@ def test_walk_group_invariance(BH, cfg, group):
     b = BH(m, p, v, walk_group=group, **prm)
     b.build_tree()
     got = b.compute_forces()
-    assert np.array_equal(got, ref)
     assert np.array_equal(a.get_interactions()[0], b.get_interactions()[0])
+    assert relerr(got, ref).max() < 1e-5
+    o = _oracle(m, p, v, prm)
+    oacc, ocnt = o.forces()
+    assert np.array_equal(b.get_interactions()[0].astype(np.int64), ocnt)
+    assert relerr(got, oacc).max() < TOL
 
 
-@pytest.mark.parametrize("cfg,group,variant", [("cfg3", 68, ""), ("cfg3", 67, ""), ("cfg3", 1, ""),
-                                               ("cfg3", 83, ""), ("cfg5", 68, ""), ("cfg3", 68, "massless"),
+@pytest.mark.parametrize("cfg,group,variant", [("cfg3", 68, ""), ("cfg3", 67, ""), ("cfg3", 66, ""),
+                                               ("cfg5", 68, ""), ("cfg3", 68, "massless"),
                                                ("cfg3", 68, "scaled")])
 def test_containment_fold_vs_test(BH, cfg, group, variant, monkeypatch):
     """theta >= 0.57: containment folded into T_acc through the nodes' bounding
@@ -677,11 +683,12 @@ def test_quadrupole_parity(BH, cfg, n):
     e_q = np.median(relerr(acc[tg], ref))
     e_m = np.median(relerr(am[tg], ref))
     assert e_q < 0.5 * e_m, (e_q, e_m)
-    # every walk variant that supports it gives bitwise the same forces
-    for g in (1, 32, 64, 66, 67, 68, 70):
+    # every group size: the same counts, forces to rounding
+    for g in (66, 67, 68):
         b = BH(m, p, v, multipole=2, walk_group=g, **prm)
         b.build_tree()
-        assert np.array_equal(b.compute_forces(), acc), g
+        assert relerr(b.compute_forces(), acc).max() < 1e-5, g
+        assert np.array_equal(b.get_interactions()[0], bh.get_interactions()[0]), g
     bh.step(2)
     o.step(2)
     assert relerr(bh.get_state()[0], o.state()[0]).max() < TOL
@@ -695,7 +702,7 @@ def test_quadrupole_arg_checks(BH):
         BH(m, p, v, theta=0.5, eps=1e-3, multipole=3)
     assert e.value.code == -1
     with pytest.raises(BhError) as e:
-        BH(m, p, v, theta=0.5, eps=1e-3, multipole=2, walk_group=80)
+        BH(m, p, v, theta=0.5, eps=1e-3, multipole=2, walk_group=80)  # not a walk_group code
     assert e.value.code == -1
     b = BH(m, p, v, theta=0.5, eps=1e-3)
     b.build_tree()

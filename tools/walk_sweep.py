@@ -1,6 +1,6 @@
 """Walk-kernel sweep: device time of K6 per traversal-group size (and phase times).
 
-    python tools/walk_sweep.py [--config cfg4] [--groups 32,16,8,4,2,1] [--reps 3]
+    python tools/walk_sweep.py [--config cfg4] [--groups 68,67,66] [--reps 3]
 
 Prints one JSON line per group size: walk ms (CUDA events on the ctx stream),
 interactions, opens, MAC fallbacks, interactions/s and useful FP32 TFLOP/s.
@@ -19,9 +19,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--n", type=int, default=0)
-    ap.add_argument("--groups", default="32,16,8,4,2,1")
+    ap.add_argument("--groups", default="68,67,66")
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--levels", action="store_true")
     a = ap.parse_args()
     from paper_1109_5190_b200 import BarnesHut
 
@@ -35,12 +34,6 @@ def main():
         bh.compute_forces(_dev_out(bh))
         bh.sync()
         st_stats = bh.get_stats()
-        if a.levels:
-            it, ac, ia = bh.get_walk_level_stats()
-            for l in range(24):
-                if it[l]:
-                    print(f"  level {l:2d}: slots {it[l]:.3e} active {ac[l]/it[l]:.3f} inter {ia[l]/it[l]:.3f} "
-                          f"share-of-slots {it[l]/it.sum():.3f} share-of-inter {ia[l]/ia.sum():.3f}", flush=True)
         bh.set_walk_stats(False)
         bh.sync()
         bh.set_profiling(True)
@@ -52,7 +45,7 @@ def main():
         fl = 18 * st["interactions"] + 8 * st_stats["opens"]
         print(json.dumps({"config": a.config, "n": int(m.shape[0]), "group": g, "walk_ms": ms,
                           "interactions": st["interactions"], "opens": st_stats["opens"], "redo": st["redo_targets"],
-                          "fallbacks": st["mac_fallbacks"], "simd_eff": (st_stats["interactions"] + st_stats["opens"]) / max(1, st_stats["lane_iters"]), "inter_per_s": st["interactions"] / ms * 1e3,
+                          "fallbacks": st["mac_fallbacks"], "inter_per_s": st["interactions"] / ms * 1e3,
                           "tflops": fl / ms / 1e9}), flush=True)
         bh.close()
 
