@@ -105,7 +105,7 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
   L.sort_tiles = (n + SORT_TILE - 1) / SORT_TILE;
   L.scan_tiles = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
   L.blocks = (n + 1 + 255) / 256;  // tree.cu's particle blocks
-  size_t sz[32] = {
+  size_t sz[31] = {
       sizeof(DevStatus),                       // 0 status
       (size_t)n * 16,                          // 1 pos4
       (size_t)L.n_own_max * 16,                // 2 vel4
@@ -137,10 +137,9 @@ Layout make_layout(int64_t n, int world, int64_t node_capacity, int multipole) {
       multipole == 2 ? (size_t)L.cap_rec * 48 : 0,  // 28 lvl_q
       (size_t)BH_NLEVELS * (L.blocks + (L.blocks + 1023) / 1024) * 4,  // 29 blkcnt + segment sums (tree.cu)
       (size_t)L.cap_rec * 4,                   // 30 lvl_rad: bounding radius of each item (containment fold)
-      (size_t)BH_NLEVELS * ((n + 4095) / 4096 + 1) * 4,  // 31 K5 straggler queues (com.cu, MOM_CHUNK 4096)
   };
   size_t off = 0;
-  for (int i = 0; i < 32; i++) {
+  for (int i = 0; i < 31; i++) {
     L.off[i] = off;
     off += align_up(sz[i]);
   }
@@ -182,7 +181,6 @@ void bind_workspace(const Layout &L, void *base, Workspace &W) {
   W.lvl_rad = (float *)(b + L.off[30]);
   W.redo = (uint32_t *)(b + L.off[21]);
   W.gcost = (uint32_t *)(b + L.off[22]);
-  W.mom_strag = (uint32_t *)(b + L.off[31]);
   W.qmom = L.off[23] != L.off[24] ? (double *)(b + L.off[23]) : nullptr;
   W.qrec = L.off[24] != L.off[25] ? (float4 *)(b + L.off[24]) : nullptr;
 }
@@ -320,8 +318,8 @@ static bh_status validate(const bh_params *p, char *err, size_t errn) {
     return BH_ERR_ARG;
   }
   int g = p->walk_group;
-  if (!(g == 0 || g == 66 || g == 67 || g == 68)) {
-    snprintf(err, errn, "walk_group must be 0 (automatic), 66, 67 or 68");
+  if (!(g == 0 || (g >= 66 && g <= 70))) {
+    snprintf(err, errn, "walk_group must be 0 (automatic) or 66..70");
     return BH_ERR_ARG;
   }
   return BH_OK;
@@ -436,12 +434,13 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   memset(&a, 0, sizeof a);
   a.n = n;
   a.buf = ctx->sort_buf;
-  // walk_group 0 = automatic: 4-target groups (2 lanes x 2 targets) unless the
-  // walks are long (theta < 0.6 on n >= 2^22: ~2000 interactions per target),
-  // where 8-target groups amortise the shared loads better (measured on the
-  // BASELINE configs)
+  // walk_group 0 = automatic: 4-target groups (2 lanes x 2 targets, code 68)
+  // unless the walks are long (theta < 0.6 on n >= 2^22: ~2000 interactions
+  // per target), where 8-target groups of 2 lanes x 4 targets (code 69) halve
+  // the record bytes per target-visit (measured on the BASELINE configs,
+  // DESIGN.md §5)
   a.group = ctx->p.walk_group != 0 ? ctx->p.walk_group
-                                   : ((ctx->p.theta < 0.6 && n >= ((int64_t)1 << 22)) ? 67 : 68);
+                                   : ((ctx->p.theta < 0.6 && n >= ((int64_t)1 << 22)) ? 69 : 68);
   a.stats = ctx->walk_stats;
   a.num_sms = ctx->num_sms;
   // containment test elision (see walk.cu): a cell holding the target has

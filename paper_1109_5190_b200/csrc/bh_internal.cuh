@@ -68,7 +68,6 @@ struct DevStatus {
   float L;
   float scale;
   uint32_t pad[3];
-  uint32_t mom_strag[24];   // K5: non-local nodes queued per level (com.cu k_moments_local; zeroed by K4)
   uint32_t lvl_count[24];   // items (records) per level 0..22; [23] = 0
   uint32_t lvl_offset[24];  // exclusive prefix of lvl_count (level-ordered item arrays)
 };
@@ -105,7 +104,6 @@ struct Workspace {
   uint32_t *targets;  // world > 1: the walk groups holding an own particle (walk.cu)
   uint32_t *redo;     // target slots whose fp32 MAC filter was inconclusive
   uint32_t *gcost;      // per storage id: loop trips of its walk group in the last walk (group order)
-  uint32_t *mom_strag;  // K5 straggler queues: [level][chunks + 1] item indices (com.cu)
   double *qmom;       // multipole = 2: per record, fp64 quadrupole xx yy zz xy xz yz (null otherwise)
   float4 *qrec;       // multipole = 2: per record, 2 float4 = fp32 (xx yy zz xy) (xz yz 0 0)
   uint32_t *scan_tmp; // scan tile partials
@@ -133,7 +131,7 @@ struct Workspace {
 struct Layout {
   int64_t n, cap_rec, cap_int, n_own_max, sort_tiles, scan_tiles, cap_resume, blocks;
   size_t total;
-  size_t off[33];
+  size_t off[32];
 };
 
 // radix sort geometry (sort.cu)

@@ -250,76 +250,11 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
   rec[c] = r;
 }
 
-// K5 in one pass for the nodes that lie inside a chunk of MOM_CHUNK
-// consecutive particles (almost all of them), levels 22 .. 0 bottom-up inside
-// the block.  The block's items of level l are those whose first particle is
-// in the chunk: the index range [rank_l(P0), rank_l(P1)) from K4's per-block
-// item offsets.  A node is local iff its last child is (its children are the
-// contiguous next-level items [clo(t), clo(t+1)), the first of which starts at
-// the node's first particle >= P0); particles are local.  Local flags of the
-// previous level sit in shared memory; a local node is summed here with the
-// very same moments_node (bit-identical results), a non-local one is queued
-// for its level's straggler launch (k_moments_level over the queue, after all
-// of the level below).  22 dependent level launches over every item become one
-// streaming pass plus 22 launches over ~one node per chunk boundary and level.
-constexpr int MOM_CHUNK = 4096;  // particles per block (a multiple of tree.cu's 256-particle blocks)
-template <bool QUAD, bool FOLD>
-__global__ void __launch_bounds__(256) k_moments_local(int64_t n, DevStatus *__restrict__ st,
-                                                       const uint32_t *__restrict__ item_rec,
-                                                       const uint32_t *__restrict__ item_clo,
-                                                       uint32_t *__restrict__ lvl_skip, double4 *__restrict__ lvl_mom,
-                                                       Rec *__restrict__ rec, double theta, double *__restrict__ lvl_q,
-                                                       double *__restrict__ qmom, float4 *__restrict__ qrec,
-                                                       const ContFold cf, const uint32_t *__restrict__ blkcnt,
-                                                       int64_t nblk, int64_t nseg, uint32_t *__restrict__ strag,
-                                                       int64_t strag_stride) {
-  __shared__ uint8_t flag[2][MOM_CHUNK];
-  __shared__ uint32_t s_lo[BH_NLEVELS], s_hi[BH_NLEVELS], s_off[BH_NLEVELS], s_cnt[BH_NLEVELS + 1];
-  if (st->err & ERR_NODE_OVERFLOW) return;
-  const int64_t P0 = (int64_t)blockIdx.x * MOM_CHUNK;
-  const int64_t P1 = P0 + MOM_CHUNK < n ? P0 + MOM_CHUNK : n;
-  const uint32_t *segsum = blkcnt + (int64_t)BH_NLEVELS * nblk;
-  if (threadIdx.x < BH_NLEVELS) {
-    const int l = threadIdx.x;
-    auto rank = [&](int64_t p) -> uint32_t {  // level-l items whose first particle is < p (p a multiple of 256)
-      const int64_t k = p / 256;
-      return blkcnt[l * nblk + k] + segsum[l * nseg + k / LS_SEG];
-    };
-    s_lo[l] = rank(P0);
-    s_hi[l] = P1 == n ? st->lvl_count[l] : rank(P1);
-    s_off[l] = st->lvl_offset[l];
-    s_cnt[l] = st->lvl_count[l];
-  }
-  if (threadIdx.x == 0) s_cnt[BH_NLEVELS] = 0;
-  __syncthreads();
-  const double Ld = (double)st->L;
-  for (int l = BH_NLEVELS - 1; l >= 0; l--) {
-    const uint32_t lo = s_lo[l], hi = s_hi[l], off = s_off[l], cnt = s_cnt[l];
-    const int cur = l & 1;
-    for (uint32_t t = lo + threadIdx.x; t < hi; t += blockDim.x) {
-      const uint32_t e = item_rec[off + t];
-      uint8_t f = 1;
-      if (!(e & ITEM_LEAF)) {  // (level 22 holds bucket members only)
-        const uint32_t clo = item_clo[off + t];
-        const uint32_t chi = t + 1 < cnt ? item_clo[off + t + 1] : s_cnt[l + 1];
-        const uint32_t last = chi - 1, lo1 = s_lo[l + 1];
-        f = last < s_hi[l + 1] ? flag[cur ^ 1][last - lo1] : (uint8_t)0;
-        if (f) {
-          moments_node<QUAD, FOLD>(l, t, e, clo, chi, off, s_off[l + 1], Ld, theta, item_rec, lvl_skip, lvl_mom,
-                                   rec, lvl_q, qmom, qrec, cf, st);
-        } else {
-          const uint32_t k = atomicAdd(&st->mom_strag[l], 1u);
-          strag[l * strag_stride + k] = t;
-        }
-      }
-      flag[cur][t - lo] = f;
-    }
-    __syncthreads();
-  }
-}
-
-// one launch per level: the level's straggler queue (k_moments_local) or,
-// with a null queue, every item of the level
+// one launch per level over the level's items (a node after its children).
+// (Measured alternative, not kept: one chunk-local pass over the nodes inside
+// 4096-particle chunks plus per-level launches over the boundary nodes -- cfg4
+// 0.83 vs 0.64 ms, cfg5 4.05 vs 3.56 ms: the per-chunk level loop is latency
+// bound, profiles/r2_summary.md.)
 template <bool QUAD, bool FOLD>
 __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__restrict__ st,
                                                        const uint32_t *__restrict__ item_rec,
@@ -328,26 +263,13 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
                                                        double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
                                                        double theta,
                                                        double *__restrict__ lvl_q, double *__restrict__ qmom,
-                                                       float4 *__restrict__ qrec, const ContFold cf,
-                                                       const uint32_t *__restrict__ queue) {
+                                                       float4 *__restrict__ qrec, const ContFold cf) {
   if (st->err & ERR_NODE_OVERFLOW) return;
-  const uint32_t cnt_all = st->lvl_count[level];
-  const uint32_t cnt = queue ? st->mom_strag[level] : cnt_all;
+  const uint32_t cnt = st->lvl_count[level];
   const uint32_t off = st->lvl_offset[level];
   const uint32_t cnt1 = st->lvl_count[level + 1];
   const uint32_t off1 = st->lvl_offset[level + 1];
   const double Ld = (double)st->L;
-  if (queue) {  // the stragglers: one node per thread
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-      const uint32_t t = queue[k];
-      const uint32_t e = item_rec[off + t];
-      const uint32_t lo = item_clo[off + t];
-      const uint32_t hi = t + 1 < cnt_all ? item_clo[off + t + 1] : cnt1;
-      moments_node<QUAD, FOLD>(level, t, e, lo, hi, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec, lvl_q,
-                               qmom, qrec, cf, st);
-    }
-    return;
-  }
   // one round trip for an item, one for its children (loads hoisted so they
   // are in flight together); the next item's loads are issued before this
   // one's children are summed
@@ -384,32 +306,16 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont
   cf.lvl_rad = W.lvl_rad;
   cf.on = cont_fold;
   if (n < 2) return cudaSuccess;
-  const int64_t nblk = (n + 1 + 255) / 256;  // tree.cu's particle blocks
-  const int64_t nseg = (nblk + LS_SEG - 1) / LS_SEG;
-  const int64_t chunks = (n + MOM_CHUNK - 1) / MOM_CHUNK;
-  const int64_t stride = chunks + 1;  // stragglers per level <= one per chunk
-#define BH_MOM_LOCAL(Q, F)                                                                                     \
-  k_moments_local<Q, F><<<(unsigned)chunks, 256, 0, s>>>(n, W.status, W.item_rec, W.item_clo, W.lvl_skip,       \
-                                                         W.lvl_mom, W.rec, theta, W.lvl_q, W.qmom, W.qrec, cf,  \
-                                                         W.blkcnt, nblk, nseg, W.mom_strag, stride)
-  if (W.qmom) {
-    if (cf.on) BH_MOM_LOCAL(true, true);
-    else BH_MOM_LOCAL(true, false);
-  } else {
-    if (cf.on) BH_MOM_LOCAL(false, true);
-    else BH_MOM_LOCAL(false, false);
-  }
-#undef BH_MOM_LOCAL
-  if (launches) (*launches)++;
-  // the stragglers, level by level (a node after its children)
-  int64_t need = (chunks + 255) / 256;
-  int grid = (int)(need < 148 ? need : 148);
+  // grid: enough blocks for the widest level (at most n items), capped at 8
+  // waves of 148 SMs
+  int64_t need = (n + 255) / 256;
+  int64_t lim = 148 * 8;
+  int grid = (int)(need < lim ? need : lim);
   if (grid < 1) grid = 1;
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
-    const uint32_t *q = W.mom_strag + l * stride;
 #define BH_MOM_LAUNCH(Q, F)                                                                                  \
   k_moments_level<Q, F><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom, W.rec, \
-                                             theta, W.lvl_q, W.qmom, W.qrec, cf, q)
+                                             theta, W.lvl_q, W.qmom, W.qrec, cf)
     if (W.qmom) {
       if (cf.on) BH_MOM_LAUNCH(true, true);
       else BH_MOM_LAUNCH(true, false);

@@ -155,7 +155,6 @@ __global__ void k_lvl_offsets(const uint32_t *__restrict__ nstart, int64_t n, in
                               Rec *__restrict__ rec, float4 *__restrict__ qrec) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint32_t run = 0;
-  for (int l = 0; l < 24; l++) st->mom_strag[l] = 0;  // K5's straggler queues (com.cu)
   for (int l = 0; l < BH_NLEVELS; l++) {
     st->lvl_offset[l] = run;
     run += st->lvl_count[l];

@@ -30,31 +30,37 @@ namespace bh {
 #ifndef BH_WALK_UNROLL
 #define BH_WALK_UNROLL 2  // record visits per loop trip, groups of >= 4 lanes
 #endif
+#ifndef BH_WALK_UNROLL_NP2
+#define BH_WALK_UNROLL_NP2 3  // 4 targets per lane
+#endif
 #ifndef BH_WALK_UNROLL_SMALL
 #define BH_WALK_UNROLL_SMALL 3  // groups of <= 2 lanes (3 vs 2: cfg5 -2.2%, cfg3 -1.2%, cfg2 -1.4%, r1)
 #endif
 // Accumulation: every target's contributions are summed in fp32 over blocks
 // of BH_FOLD_TRIPS loop trips of its group's walk, and each block is folded
-// into an outer sum (BH_FOLD = 1: fp32, 2: fp64, 0: one fp32 sum).  The trip
-// counter is uniform over the warp (a non-divergent branch), and the blocks --
-// hence the rounding -- depend only on the group's own walk (the same at any
-// rank count: world > 1 walks the P = 1 groups).  Measured on all 2^24 cfg4
-// targets (profiles/r2_accuracy.md): max relative error 1.26e-4 with one fp32
-// sum, 1.45e-5 with BH_FOLD 1, 6.5e-6 with BH_FOLD 2 (+6% / +15% walk time).
+// into an outer sum: fold mode 1 = fp32 outer sums in registers (NP = 1),
+// 3 = fp32 outer sums in shared memory (NP = 2, whose registers are full),
+// 2 = fp64 in registers, 0 = one fp32 sum.  The trip counter is uniform over
+// the warp (a non-divergent branch), and the blocks -- hence the rounding --
+// depend only on the group's own walk (the same at any rank count: world > 1
+// walks the P = 1 groups).  Measured on all 2^24 cfg4 targets
+// (profiles/r2_summary.md): max relative error 1.26e-4 with one fp32 sum,
+// 1.45e-5 with fp32 block sums (8-target groups of 4 lanes x 2), 2.2e-5
+// (2 lanes x 4), 6.5e-6 with fp64 outer sums.
 #ifndef BH_FOLD
-#define BH_FOLD 1
+#define BH_FOLD 1      // NP = 1 (0 / 1 / 2)
 #endif
-#ifndef BH_OPN_MIN
-#define BH_OPN_MIN 1
+#ifndef BH_FOLD_NP2
+#define BH_FOLD_NP2 3  // NP = 2 (0 / 1 / 3)
 #endif
 #ifndef BH_FOLD_TRIPS
 #define BH_FOLD_TRIPS 16
 #endif
-#if BH_FOLD == 2
-typedef double FoldT;
-#else
-typedef float FoldT;
+#ifndef BH_WALK_MINB2
+#define BH_WALK_MINB2 8  // NP = 2 (4 targets per lane): 64 registers
 #endif
+template <int FM> struct FoldType { typedef float T; };
+template <> struct FoldType<2> { typedef double T; };
 
 // One target's MAC at record cc (see the header comment); with QUAD the
 // quadrupole factors of a target that does not accept are zeroed too.
@@ -87,9 +93,9 @@ __device__ __forceinline__ void mac_one(uint32_t cc, float d2, float tacc, float
 }
 
 // STATS: also count the opened MAC tests (the flop model of bench.py).
-template <int GL, bool CONT, bool QUAD, bool STATS>
-__global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : BH_WALK_MINB) k_walk(const WalkParams P) {
-  constexpr int TPL = 2;                   // targets per lane (one packed pair)
+template <int GL, int NP, bool CONT, bool QUAD, bool STATS>
+__global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_MINB : BH_WALK_MINB2)) k_walk(const WalkParams P) {
+  constexpr int TPL = 2 * NP;              // targets per lane (NP packed pairs)
   constexpr int GT = GL * TPL;             // targets per group
   constexpr int GPB = BH_WALK_BLOCK / GL;  // groups per block
   const uint32_t full = 0xffffffffu;
@@ -159,8 +165,16 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : BH_WALK_MINB) k_walk
     nop[k] = 0;
     ax[k] = ay[k] = az[k] = 0.f;
   }
-  const F2 X = pk2(T[0].me.x, T[1].me.x), Y = pk2(T[0].me.y, T[1].me.y), Z = pk2(T[0].me.z, T[1].me.z);
-  const uint32_t LiA = T[0].Li, LiB = T[1].Li;
+  F2 X[NP], Y[NP], Z[NP];
+  uint32_t Li[TPL];
+#pragma unroll
+  for (int j = 0; j < NP; j++) {
+    X[j] = pk2(T[2 * j].me.x, T[2 * j + 1].me.x);
+    Y[j] = pk2(T[2 * j].me.y, T[2 * j + 1].me.y);
+    Z[j] = pk2(T[2 * j].me.z, T[2 * j + 1].me.z);
+  }
+#pragma unroll
+  for (int k = 0; k < TPL; k++) Li[k] = T[k].Li;
   const F2 E2 = pk2(P.eps2, P.eps2);
   const bool gvalid = (__ballot_sync(full, anyv) & gmask) != 0u;
   const Rec *__restrict__ rec = P.rec;
@@ -168,100 +182,99 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : BH_WALK_MINB) k_walk
   asm volatile("" : "+r"(gmask2));  // a plain register: the group test is one LOP3
   uint32_t c = gvalid ? 0u : Wn;
   uint32_t git = 0;  // live loop trips of this lane's group (its cost; visits per trip = the unroll)
-#if BH_FOLD
-  FoldT ox[TPL], oy[TPL], oz[TPL];
+  constexpr int FM = NP == 1 ? BH_FOLD : BH_FOLD_NP2;  // fold mode
+  typedef typename FoldType<FM>::T FoldT;
+  // FM 1 / 2: the outer sums in registers; FM 3: in shared memory, [3 TPL][BLOCK]
+  FoldT ox[FM == 1 || FM == 2 ? TPL : 1], oy[FM == 1 || FM == 2 ? TPL : 1], oz[FM == 1 || FM == 2 ? TPL : 1];
+  __shared__ float s_out[FM == 3 ? 3 * TPL : 1][FM == 3 ? BH_WALK_BLOCK : 1];
+  if constexpr (FM == 1 || FM == 2) {
 #pragma unroll
-  for (int k = 0; k < TPL; k++) ox[k] = oy[k] = oz[k] = (FoldT)0;
+    for (int k = 0; k < TPL; k++) ox[k] = oy[k] = oz[k] = (FoldT)0;
+  }
+  if constexpr (FM == 3) {
+#pragma unroll
+    for (int k = 0; k < 3 * TPL; k++) s_out[k][threadIdx.x] = 0.f;
+  }
   uint32_t trip = 0;
-#endif
   if (__any_sync(full, c < Wn)) for (;;) {
 #pragma unroll
-    for (int u = 0; u < (GL <= 2 ? BH_WALK_UNROLL_SMALL : BH_WALK_UNROLL); u++) {
+    for (int u = 0; u < (NP == 2 ? BH_WALK_UNROLL_NP2 : GL <= 2 ? BH_WALK_UNROLL_SMALL : BH_WALK_UNROLL); u++) {
       const uint32_t cc = c;
       float4 cm;
       uint4 au;
       ld_rec(rec + cc, cm, au);
       const uint32_t skip = au.z, dropw = au.w;
       const float tacc = __uint_as_float(au.x), trej = __uint_as_float(au.y);
-      const F2 DX = sub2(pk2(cm.x, cm.x), X), DY = sub2(pk2(cm.y, cm.y), Y), DZ = sub2(pk2(cm.z, cm.z), Z);
-      const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
-      float d2A, d2B;
-      up2(D2, d2A, d2B);
-      // the interaction of both targets, branch-free (f zeroed for a target
-      // that does not accept the record)
-      float r2A, r2B;
-      up2(add2(D2, E2), r2A, r2B);
-      const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
-      float fA, fB;
-      const F2 INV2 = mul2(INV, INV);
-      up2(mul2(mul2(pk2(cm.w, cm.w), INV2), INV), fA, fB);
-      // multipole = 2: the record's -Q (broadcast) and the quadrupole factors
-      // (quad_term's operation sequence, in pairs)
-      F2 QX, QY, QZ;
-      float g1A = 0.f, g1B = 0.f, g2A = 0.f, g2B = 0.f;
-      if (QUAD) {
-        const float4 qa = __ldg(&P.qrec[2 * (size_t)cc]), qb = __ldg(&P.qrec[2 * (size_t)cc + 1]);
-        // qa = (xx, yy, zz, xy), qb = (xz, yz, -, -)
-        QX = fma2(pk2(qb.x, qb.x), DZ, fma2(pk2(qa.w, qa.w), DY, mul2(pk2(qa.x, qa.x), DX)));
-        QY = fma2(pk2(qb.y, qb.y), DZ, fma2(pk2(qa.y, qa.y), DY, mul2(pk2(qa.w, qa.w), DX)));
-        QZ = fma2(pk2(qa.z, qa.z), DZ, fma2(pk2(qb.y, qb.y), DY, mul2(pk2(qb.x, qb.x), DX)));
-        const F2 SQ = fma2(QZ, DZ, fma2(QY, DY, mul2(QX, DX)));
-        const F2 INV5 = mul2(mul2(INV2, INV2), INV);
-        const F2 INV7 = mul2(INV5, INV2);
-        up2(INV5, g1A, g1B);
-        up2(mul2(mul2(pk2(-2.5f, -2.5f), SQ), INV7), g2A, g2B);
-      }
-      // per-target MAC; a record containing the target is opened, never
-      // accepted (CONT: NaN distance)
-      float qA = d2A, qB = d2B;
-      if (CONT) {
-        const bool cA = (cc <= LiA) & (skip > LiA), cB = (cc <= LiB) & (skip > LiB);
-        const float qnan = __int_as_float(0x7fffffff);
-        qA = cA ? qnan : d2A;
-        qB = cB ? qnan : d2B;
-      }
-#if !BH_OPN_MIN
-      // (variant: the open test from the pre-update state, off the SEL chain)
-      uint32_t opn_pred;
-      asm("{\n\t.reg .pred pa, pb, po;\n\t"
-          "setp.ge.u32 pa, %1, %2;\n\t"
-          "setp.ge.u32 pb, %1, %3;\n\t"
-          "setp.ltu.and.f32 pa, %4, %6, pa;\n\t"
-          "setp.ltu.and.f32 pb, %5, %6, pb;\n\t"
-          "or.pred po, pa, pb;\n\t"
-          "selp.u32 %0, 1, 0, po;\n\t}"
-          : "=r"(opn_pred) : "r"(cc), "r"(res[0]), "r"(res[1]), "f"(qA), "f"(qB), "f"(trej));
-#endif
-      mac_one<QUAD>(cc, qA, tacc, trej, skip, dropw, res[0], cnt[0], fA, g1A, g2A);
-      mac_one<QUAD>(cc, qB, tacc, trej, skip, dropw, res[1], cnt[1], fB, g1B, g2B);
-      const F2 FF = pk2(fA, fB);
-      // packed accumulate on (a, b) register pairs (this form avoids ptxas moves)
-      asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
-          : "+f"(ax[0]), "+f"(ax[1]) : "l"(FF.v), "l"(DX.v));
-      asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
-          : "+f"(ay[0]), "+f"(ay[1]) : "l"(FF.v), "l"(DY.v));
-      asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
-          : "+f"(az[0]), "+f"(az[1]) : "l"(FF.v), "l"(DZ.v));
-      if (QUAD) {
-        const F2 G1 = pk2(g1A, g1B), G2 = pk2(g2A, g2B);
-        F2 AX = pk2(ax[0], ax[1]), AY = pk2(ay[0], ay[1]), AZ = pk2(az[0], az[1]);
-        AX = fma2(G2, DX, fma2(G1, QX, AX));
-        AY = fma2(G2, DY, fma2(G1, QY, AY));
-        AZ = fma2(G2, DZ, fma2(G1, QZ, AZ));
-        up2(AX, ax[0], ax[1]);
-        up2(AY, ay[0], ay[1]);
-        up2(AZ, az[0], az[1]);
+#pragma unroll
+      for (int j = 0; j < NP; j++) {
+        const int ka = 2 * j, kb = 2 * j + 1;
+        const F2 DX = sub2(pk2(cm.x, cm.x), X[j]), DY = sub2(pk2(cm.y, cm.y), Y[j]), DZ = sub2(pk2(cm.z, cm.z), Z[j]);
+        const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
+        float d2A, d2B;
+        up2(D2, d2A, d2B);
+        // the interaction of both targets, branch-free (f zeroed for a target
+        // that does not accept the record)
+        float r2A, r2B;
+        up2(add2(D2, E2), r2A, r2B);
+        const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
+        float fA, fB;
+        const F2 INV2 = mul2(INV, INV);
+        up2(mul2(mul2(pk2(cm.w, cm.w), INV2), INV), fA, fB);
+        // multipole = 2: the record's -Q (broadcast) and the quadrupole factors
+        // (quad_term's operation sequence, in pairs)
+        F2 QX, QY, QZ;
+        float g1A = 0.f, g1B = 0.f, g2A = 0.f, g2B = 0.f;
+        if (QUAD) {
+          const float4 qa = __ldg(&P.qrec[2 * (size_t)cc]), qb = __ldg(&P.qrec[2 * (size_t)cc + 1]);
+          // qa = (xx, yy, zz, xy), qb = (xz, yz, -, -)
+          QX = fma2(pk2(qb.x, qb.x), DZ, fma2(pk2(qa.w, qa.w), DY, mul2(pk2(qa.x, qa.x), DX)));
+          QY = fma2(pk2(qb.y, qb.y), DZ, fma2(pk2(qa.y, qa.y), DY, mul2(pk2(qa.w, qa.w), DX)));
+          QZ = fma2(pk2(qa.z, qa.z), DZ, fma2(pk2(qb.y, qb.y), DY, mul2(pk2(qb.x, qb.x), DX)));
+          const F2 SQ = fma2(QZ, DZ, fma2(QY, DY, mul2(QX, DX)));
+          const F2 INV5 = mul2(mul2(INV2, INV2), INV);
+          const F2 INV7 = mul2(INV5, INV2);
+          up2(INV5, g1A, g1B);
+          up2(mul2(mul2(pk2(-2.5f, -2.5f), SQ), INV7), g2A, g2B);
+        }
+        // per-target MAC; a record containing the target is opened, never
+        // accepted (CONT: NaN distance)
+        float qA = d2A, qB = d2B;
+        if (CONT) {
+          const bool cA = (cc <= Li[ka]) & (skip > Li[ka]), cB = (cc <= Li[kb]) & (skip > Li[kb]);
+          const float qnan = __int_as_float(0x7fffffff);
+          qA = cA ? qnan : d2A;
+          qB = cB ? qnan : d2B;
+        }
+        mac_one<QUAD>(cc, qA, tacc, trej, skip, dropw, res[ka], cnt[ka], fA, g1A, g2A);
+        mac_one<QUAD>(cc, qB, tacc, trej, skip, dropw, res[kb], cnt[kb], fB, g1B, g2B);
+        const F2 FF = pk2(fA, fB);
+        // packed accumulate on (a, b) register pairs (this form avoids ptxas moves)
+        asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+            : "+f"(ax[ka]), "+f"(ax[kb]) : "l"(FF.v), "l"(DX.v));
+        asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+            : "+f"(ay[ka]), "+f"(ay[kb]) : "l"(FF.v), "l"(DY.v));
+        asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+            : "+f"(az[ka]), "+f"(az[kb]) : "l"(FF.v), "l"(DZ.v));
+        if (QUAD) {
+          const F2 G1 = pk2(g1A, g1B), G2 = pk2(g2A, g2B);
+          F2 AX = pk2(ax[ka], ax[kb]), AY = pk2(ay[ka], ay[kb]), AZ = pk2(az[ka], az[kb]);
+          AX = fma2(G2, DX, fma2(G1, QX, AX));
+          AY = fma2(G2, DY, fma2(G1, QY, AY));
+          AZ = fma2(G2, DZ, fma2(G1, QZ, AZ));
+          up2(AX, ax[ka], ax[kb]);
+          up2(AY, ay[ka], ay[kb]);
+          up2(AZ, az[ka], az[kb]);
+        }
       }
       // a target opened cc iff it was active and its res stayed <= cc
       if (STATS) {
-        nop[0] += res[0] <= cc ? 1u : 0u;
-        nop[1] += res[1] <= cc ? 1u : 0u;
+#pragma unroll
+        for (int k = 0; k < TPL; k++) nop[k] += res[k] <= cc ? 1u : 0u;
       }
-#if BH_OPN_MIN
-      const bool opn = min(res[0], res[1]) <= cc;
-#else
-      const bool opn = opn_pred != 0u;
-#endif
+      uint32_t rmin = res[0];
+#pragma unroll
+      for (int k = 1; k < TPL; k++) rmin = min(rmin, res[k]);
+      const bool opn = rmin <= cc;
       if (GL == 32) {
         c = __any_sync(full, opn) ? cc + 1u : skip;
       } else {
@@ -270,32 +283,42 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : BH_WALK_MINB) k_walk
     }
     const bool live = c < Wn;
     git += live ? 1u : 0u;
-#if BH_FOLD
-    if (++trip == BH_FOLD_TRIPS) {  // warp-uniform
-      trip = 0;
+    if constexpr (FM != 0) {
+      if (++trip == BH_FOLD_TRIPS) {  // warp-uniform
+        trip = 0;
 #pragma unroll
-      for (int k = 0; k < TPL; k++) {
-        ox[k] += (FoldT)ax[k];
-        oy[k] += (FoldT)ay[k];
-        oz[k] += (FoldT)az[k];
-        ax[k] = ay[k] = az[k] = 0.f;
+        for (int k = 0; k < TPL; k++) {
+          if constexpr (FM == 3) {
+            s_out[3 * k][threadIdx.x] += ax[k];
+            s_out[3 * k + 1][threadIdx.x] += ay[k];
+            s_out[3 * k + 2][threadIdx.x] += az[k];
+          } else {
+            ox[k] += (FoldT)ax[k];
+            oy[k] += (FoldT)ay[k];
+            oz[k] += (FoldT)az[k];
+          }
+          ax[k] = ay[k] = az[k] = 0.f;
+        }
       }
     }
-#endif
     if (!__any_sync(full, live)) break;
   }
   double dax[TPL], day[TPL], daz[TPL];
 #pragma unroll
   for (int k = 0; k < TPL; k++) {
-#if BH_FOLD
-    dax[k] = (double)ox[k] + (double)ax[k];
-    day[k] = (double)oy[k] + (double)ay[k];
-    daz[k] = (double)oz[k] + (double)az[k];
-#else
-    dax[k] = (double)ax[k];
-    day[k] = (double)ay[k];
-    daz[k] = (double)az[k];
-#endif
+    if constexpr (FM == 3) {
+      dax[k] = (double)s_out[3 * k][threadIdx.x] + (double)ax[k];
+      day[k] = (double)s_out[3 * k + 1][threadIdx.x] + (double)ay[k];
+      daz[k] = (double)s_out[3 * k + 2][threadIdx.x] + (double)az[k];
+    } else if constexpr (FM == 1 || FM == 2) {
+      dax[k] = (double)ox[k] + (double)ax[k];
+      day[k] = (double)oy[k] + (double)ay[k];
+      daz[k] = (double)oz[k] + (double)az[k];
+    } else {
+      dax[k] = (double)ax[k];
+      day[k] = (double)ay[k];
+      daz[k] = (double)az[k];
+    }
   }
   if (P.gcost) {
 #pragma unroll
@@ -357,8 +380,10 @@ __global__ void k_own_group_compact(const uint32_t *__restrict__ pre, uint32_t *
   if (g == ng) *count = pre[ng];
 }
 
-// walk_group code -> lanes per group (66: 8, 67: 4, 68: 2)
-int walk_lanes(int group) { return group == 66 ? 8 : group == 68 ? 2 : 4; }
+// walk_group code -> lanes per group and targets per lane (66 / 67 / 68: 8 /
+// 4 / 2 lanes x 2 targets; 69 / 70: 2 / 1 lanes x 4 targets)
+int walk_lanes(int group) { return group == 66 ? 8 : group == 68 || group == 69 ? 2 : group == 70 ? 1 : 4; }
+static int walk_tpl(int group) { return group == 69 || group == 70 ? 4 : 2; }
 
 cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
@@ -394,7 +419,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.own_hi = a.own_hi;
   P.own_check = a.own_check;
   P.num_sms = a.num_sms > 0 ? a.num_sms : 148;
-  const int GL = walk_lanes(a.group), GT = 2 * GL;
+  const int GL = walk_lanes(a.group), GT = walk_tpl(a.group) * GL;
   const int64_t ng_all = (a.n + GT - 1) / GT;
   int64_t ng_max = ng_all;
   P.group_list = nullptr;
@@ -418,28 +443,30 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
     constexpr int WB = BH_WALK_BLOCK;
     const unsigned grid = (unsigned)((ng_max + WB / GL - 1) / (WB / GL));
     const bool cont = a.need_cont;
-#define BH_WALK_LAUNCH(GLv)                                                      \
+#define BH_WALK_LAUNCH(GLv, NPv)                                                      \
   if (a.stats) {                                                                 \
     if (P.quad) {                                                                \
-      if (cont) k_walk<GLv, true, true, true><<<grid, WB, 0, s>>>(P);            \
-      else k_walk<GLv, false, true, true><<<grid, WB, 0, s>>>(P);                \
+      if (cont) k_walk<GLv, NPv, true, true, true><<<grid, WB, 0, s>>>(P);            \
+      else k_walk<GLv, NPv, false, true, true><<<grid, WB, 0, s>>>(P);                \
     } else {                                                                     \
-      if (cont) k_walk<GLv, true, false, true><<<grid, WB, 0, s>>>(P);           \
-      else k_walk<GLv, false, false, true><<<grid, WB, 0, s>>>(P);               \
+      if (cont) k_walk<GLv, NPv, true, false, true><<<grid, WB, 0, s>>>(P);           \
+      else k_walk<GLv, NPv, false, false, true><<<grid, WB, 0, s>>>(P);               \
     }                                                                            \
   } else {                                                                       \
     if (P.quad) {                                                                \
-      if (cont) k_walk<GLv, true, true, false><<<grid, WB, 0, s>>>(P);           \
-      else k_walk<GLv, false, true, false><<<grid, WB, 0, s>>>(P);               \
+      if (cont) k_walk<GLv, NPv, true, true, false><<<grid, WB, 0, s>>>(P);           \
+      else k_walk<GLv, NPv, false, true, false><<<grid, WB, 0, s>>>(P);               \
     } else {                                                                     \
-      if (cont) k_walk<GLv, true, false, false><<<grid, WB, 0, s>>>(P);          \
-      else k_walk<GLv, false, false, false><<<grid, WB, 0, s>>>(P);              \
+      if (cont) k_walk<GLv, NPv, true, false, false><<<grid, WB, 0, s>>>(P);          \
+      else k_walk<GLv, NPv, false, false, false><<<grid, WB, 0, s>>>(P);              \
     }                                                                            \
   }
-    switch (GL) {
-      case 8: BH_WALK_LAUNCH(8) break;
-      case 2: BH_WALK_LAUNCH(2) break;
-      default: BH_WALK_LAUNCH(4) break;
+    switch (a.group) {
+      case 66: BH_WALK_LAUNCH(8, 1) break;
+      case 68: BH_WALK_LAUNCH(2, 1) break;
+      case 69: BH_WALK_LAUNCH(2, 2) break;
+      case 70: BH_WALK_LAUNCH(1, 2) break;
+      default: BH_WALK_LAUNCH(4, 1) break;
     }
 #undef BH_WALK_LAUNCH
   }
