@@ -269,7 +269,11 @@ def ours_arm(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(device) as clk:
         ev0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            if world > 1 and args.rebalance_every > 0 and k > 0 and k % args.rebalance_every == 0:
+                # NEXT-2: equal-cost ownership from the last walk's counts, inside the
+                # timed region (host collectives: its cost is part of the step)
+                bdist.rebalance(bh, dist, device=f"cuda:{device}")
             bh.step(1)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -462,6 +466,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true", help="N > 1: keep the even Morton-range split")
+    ap.add_argument("--rebalance-every", type=int, default=0,
+                    help="N > 1: also re-split ownership by cost every K timed steps (0: once, after warm-up)")
     ap.add_argument("--cpu-samples", type=int, default=20000)
     ap.add_argument("--ref-samples", type=int, default=8192)
     args = ap.parse_args(argv)

@@ -59,7 +59,7 @@ struct DevStatus {
   unsigned long long n_redo;         // last walk: targets re-walked with the exact fp64 MAC
   unsigned long long reserved0;
   uint32_t n_own_groups;             // world > 1: walk groups holding an own particle (walk.cu)
-  uint32_t reserved1;
+  uint32_t n_long_runs;              // equal-key runs longer than TIE_SHORT queued for k_long_runs (sort.cu)
   uint32_t near_ok;     // this build's sort came from the near-sorted path (sort.cu)
   uint32_t n_bad;       // near-sorted path: keys out of local order, sorted apart
   unsigned long long interactions_cum;  // since create / set_state
@@ -159,6 +159,30 @@ cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *fina
 cudaError_t launch_near_sort(const Workspace &W, int64_t n, cudaStream_t s);
 cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s);
 cudaError_t launch_tie_fixup(const Workspace &W, int64_t n, int buf, cudaStream_t s);
+// equal-key runs (reading L13: ties by user index): runs of <= TIE_SHORT keys
+// are insertion-sorted by the thread that finds them; longer ones are queued
+// (DevStatus.n_long_runs, the list at the start of W.accu) and sorted by
+// k_long_runs, one block per run (sort.cu)
+constexpr int TIE_SHORT = 32;
+__device__ __forceinline__ void tie_run(unsigned long long kp, int64_t p, int64_t n,
+                                        const unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+                                        const uint32_t *__restrict__ uid, DevStatus *st, uint2 *runs) {
+  int64_t e = p + 1;
+  while (e + 1 < n && e + 1 - p < TIE_SHORT && keys[e + 1] == kp) ++e;
+  if (e + 1 < n && keys[e + 1] == kp) {  // a long run: queue it
+    while (e + 1 < n && keys[e + 1] == kp) ++e;
+    const uint32_t k = atomicAdd(&st->n_long_runs, 1u);
+    runs[k] = make_uint2((uint32_t)p, (uint32_t)(e + 1 - p));
+    return;
+  }
+  for (int64_t i = p + 1; i <= e; ++i) {
+    const uint32_t vv = vals[i], u = uid[vv];
+    int64_t j = i - 1;
+    while (j >= p && uid[vals[j]] > u) { vals[j + 1] = vals[j]; --j; }
+    vals[j + 1] = vv;
+  }
+}
+cudaError_t launch_long_runs(const Workspace &W, int64_t n, int buf, cudaStream_t s);
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, int cont_fold, cudaStream_t s);
 cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont_fold, cudaStream_t s,
                            int *launches);

@@ -36,13 +36,10 @@
 #define BH_MOM_PREFETCH 2  // (2 vs 1/3/4: best on cfg4 and on cfg5 with the containment fold)
 #endif
 #ifndef BH_MOM_MINB
-#define BH_MOM_MINB 0  // 0: no minimum-blocks bound
+#define BH_MOM_MINB 4  // 64 registers: 4 blocks (32 warps) per SM (the containment fold needs 66 unbounded: 3 blocks, cfg5 moments +20%)
 #endif
-#if BH_MOM_MINB > 0
-#define BH_MOM_BOUNDS __launch_bounds__(256, BH_MOM_MINB)
-#else
-#define BH_MOM_BOUNDS __launch_bounds__(256)
-#endif
+// (multipole = 2 kernels unbounded: their quadrupole sums would spill)
+#define BH_MOM_BOUNDS __launch_bounds__(256, QUAD ? 1 : BH_MOM_MINB)
 
 namespace bh {
 

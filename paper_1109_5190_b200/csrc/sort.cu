@@ -225,23 +225,100 @@ __global__ void __launch_bounds__(SORT_BLOCK, 2) k_onesweep(const unsigned long 
   }
 }
 
-// ties: re-sort each run of equal keys by user index (insertion sort; runs are
-// rare and, after the first step, almost always already in order).
+// ties: re-sort each run of equal keys by user index (reading L13): short
+// runs in place by the thread that finds them, long ones by k_long_runs.
 __global__ void k_tie_fixup(const unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
-                            const uint32_t *__restrict__ uid, int64_t n) {
+                            const uint32_t *__restrict__ uid, int64_t n, DevStatus *st, uint2 *runs) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p + 1 >= n) return;
   unsigned long long kp = keys[p];
   if (keys[p + 1] != kp) return;
   if (p > 0 && keys[p - 1] == kp) return;
-  int64_t e = p + 1;
-  while (e + 1 < n && keys[e + 1] == kp) ++e;
-  for (int64_t i = p + 1; i <= e; ++i) {
-    uint32_t v = vals[i];
-    uint32_t u = uid[v];
-    int64_t j = i - 1;
-    while (j >= p && uid[vals[j]] > u) { vals[j + 1] = vals[j]; --j; }
-    vals[j + 1] = v;
+  tie_run(kp, p, n, keys, vals, uid, st, runs);
+}
+
+// One block per queued long run [p, p + k): order vals by uid[vals] (the user
+// indices are distinct).  Tiles of LR_TILE are bitonic-sorted in shared memory;
+// runs longer than a tile are then merged pairwise by rank (an element's place
+// in the merged run = its place in its own sorted part + the count of the other
+// part's smaller keys), ping-ponging between (uid, val) pairs in scratch and
+// vals itself (keys re-gathered from uid).  Never on the path of ordinary
+// inputs (runs need many particles in one level-21 cell); bounded work
+// O(k log k) where a single-thread insertion sort was O(k^2).
+constexpr int LR_TILE = 4096;
+__global__ void __launch_bounds__(512) k_long_runs(uint32_t *__restrict__ vals, const uint32_t *__restrict__ uid,
+                                                   const DevStatus *__restrict__ st, const uint2 *__restrict__ runs,
+                                                   uint2 *__restrict__ scratch) {
+  __shared__ uint32_t sk[LR_TILE], sv[LR_TILE];
+  const uint32_t nr = st->n_long_runs;
+  for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
+    const uint2 run = runs[r];
+    const uint32_t p = run.x, k = run.y;
+    uint32_t *v = vals + p;
+    uint2 *sc = scratch + p;  // this run's merge slots
+    // 1) sort each tile in shared memory
+    for (uint32_t t0 = 0; t0 < k; t0 += LR_TILE) {
+      const uint32_t len = min((uint32_t)LR_TILE, k - t0);
+      for (uint32_t i = threadIdx.x; i < LR_TILE; i += blockDim.x) {
+        const uint32_t vv = i < len ? v[t0 + i] : 0xffffffffu;
+        sk[i] = i < len ? uid[vv] : 0xffffffffu;
+        sv[i] = vv;
+      }
+      __syncthreads();
+      for (uint32_t size = 2; size <= LR_TILE; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+          for (uint32_t i = threadIdx.x; i < LR_TILE; i += blockDim.x) {
+            const uint32_t j = i ^ stride;
+            if (j > i) {
+              const bool up = (i & size) == 0;
+              const uint32_t a = sk[i], b = sk[j];
+              if ((a > b) == up) {
+                sk[i] = b; sk[j] = a;
+                const uint32_t t = sv[i]; sv[i] = sv[j]; sv[j] = t;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
+        if (k <= (uint32_t)LR_TILE) v[t0 + i] = sv[i];
+        else sc[t0 + i] = make_uint2(sk[i], sv[i]);
+      }
+      __syncthreads();
+    }
+    if (k <= (uint32_t)LR_TILE) continue;
+    // 2) merge sorted parts of width w pairwise: scratch -> vals -> scratch ...
+    bool in_scratch = true;
+    for (uint32_t w = LR_TILE; w < k; w <<= 1) {
+      for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const uint32_t base = i / (2 * w) * (2 * w);
+        const bool left = i - base < w;
+        const uint32_t lo = left ? base + w : base;  // the other part
+        const uint32_t hi = left ? min(base + 2 * w, k) : base + w;
+        const uint32_t key = in_scratch ? sc[i].x : uid[v[i]];
+        const uint32_t val = in_scratch ? sc[i].y : v[i];
+        uint32_t a = lo, b = hi;  // count of the other part's keys < key
+        while (a < b) {
+          const uint32_t m = (a + b) >> 1;
+          const uint32_t km = in_scratch ? sc[m].x : uid[v[m]];
+          if (km < key) a = m + 1; else b = m;
+        }
+        const uint32_t pos = base + (left ? i - base : i - base - w) + (a - lo);
+        if (hi <= lo) {  // a left part without a right partner stays in place
+          if (in_scratch) v[i] = val; else sc[i] = make_uint2(key, val);
+        } else if (in_scratch) {
+          v[pos] = val;
+        } else {
+          sc[pos] = make_uint2(key, val);
+        }
+      }
+      __syncthreads();
+      in_scratch = !in_scratch;
+    }
+    if (in_scratch)
+      for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) v[i] = sc[i].y;
+    __syncthreads();
   }
 }
 
@@ -284,10 +361,27 @@ cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// scratch layout in W.accu (12 n bytes, free during the build): the list of
+// long runs (at most n / (TIE_SHORT + 1) uint2) at the front, then n uint2
+// merge slots indexed by sorted position (8 n bytes: 8 n + 8 n / 33 < 12 n)
+static uint2 *long_run_list(const Workspace &W) { return (uint2 *)W.accu; }
+static uint2 *long_run_scratch(const Workspace &W, int64_t n) {
+  return (uint2 *)W.accu + (n / (TIE_SHORT + 1) + 2);
+}
+
+cudaError_t launch_long_runs(const Workspace &W, int64_t n, int buf, cudaStream_t s) {
+  if (n < TIE_SHORT + 1) return cudaSuccess;
+  k_long_runs<<<148, 512, 0, s>>>(W.vals[buf], W.uid, W.status, long_run_list(W), long_run_scratch(W, n));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tie_fixup(const Workspace &W, int64_t n, int buf, cudaStream_t s) {
   if (n < 2) return cudaSuccess;
-  k_tie_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.uid, n);
-  return cudaGetLastError();
+  cudaError_t e = cudaMemsetAsync(&W.status->n_long_runs, 0, sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  k_tie_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W.keys[buf], W.vals[buf], W.uid, n, W.status,
+                                                           long_run_list(W));
+  return launch_long_runs(W, n, buf, s);
 }
 
 }  // namespace bh

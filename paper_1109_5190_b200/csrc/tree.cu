@@ -47,7 +47,8 @@ __device__ __forceinline__ int shared_digits(unsigned long long a, unsigned long
 __global__ void __launch_bounds__(256) k_lcp_count(const unsigned long long *__restrict__ keys, int64_t n,
                                                    uint8_t *__restrict__ lcp, uint32_t *__restrict__ nstart,
                                                    uint32_t *__restrict__ blkcnt, int64_t nblk,
-                                                   uint32_t *__restrict__ vals, const uint32_t *__restrict__ uid) {
+                                                   uint32_t *__restrict__ vals, const uint32_t *__restrict__ uid,
+                                                   DevStatus *st, uint2 *runs) {
   __shared__ uint32_t lh[BH_NLEVELS];
   if (threadIdx.x < BH_NLEVELS) lh[threadIdx.x] = 0;
   __syncthreads();
@@ -58,18 +59,9 @@ __global__ void __launch_bounds__(256) k_lcp_count(const unsigned long long *__r
     int a = p > 0 ? shared_digits(keys[p - 1], kp) : -1;
     int b = p + 1 < n ? shared_digits(kp, keys[p + 1]) : -1;
     if (p + 1 < n) lcp[p] = (uint8_t)b;
-    // equal keys (reading L13): the run's first thread orders it by user index
-    // (insertion sort; runs are rare and short)
-    if (p + 1 < n && keys[p + 1] == kp && !(p > 0 && keys[p - 1] == kp)) {
-      int64_t e = p + 1;
-      while (e + 1 < n && keys[e + 1] == kp) ++e;
-      for (int64_t i = p + 1; i <= e; ++i) {
-        const uint32_t vv = vals[i], u = uid[vv];
-        int64_t j = i - 1;
-        while (j >= p && uid[vals[j]] > u) { vals[j + 1] = vals[j]; --j; }
-        vals[j + 1] = vv;
-      }
-    }
+    // equal keys (reading L13): the run's first thread orders a short run by
+    // user index, a long one goes to k_long_runs
+    if (p + 1 < n && keys[p + 1] == kp && !(p > 0 && keys[p - 1] == kp)) tie_run(kp, p, n, keys, vals, uid, st, runs);
     int ni = b > a ? b - a : 0;
     nstart[p] = (uint32_t)ni + 1u;
     ll = (a > b ? a : b) + 1;  // leaf level (22: bucket member)
@@ -275,8 +267,13 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
 
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, int cont_fold, cudaStream_t s) {
   const int64_t nblk = (n + 1 + 255) / 256;
-  k_lcp_count<<<(unsigned)nblk, 256, 0, s>>>(W.keys[buf], n, W.lcp, W.nstart, W.blkcnt, nblk, W.vals[buf], W.uid);
-  cudaError_t e = launch_scan_u32(W.nstart, n + 1, W.scan_tmp, s);
+  cudaError_t e = cudaMemsetAsync(&W.status->n_long_runs, 0, sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  k_lcp_count<<<(unsigned)nblk, 256, 0, s>>>(W.keys[buf], n, W.lcp, W.nstart, W.blkcnt, nblk, W.vals[buf], W.uid,
+                                            W.status, (uint2 *)W.accu);
+  e = launch_long_runs(W, n, buf, s);
+  if (e != cudaSuccess) return e;
+  e = launch_scan_u32(W.nstart, n + 1, W.scan_tmp, s);
   if (e != cudaSuccess) return e;
   const int64_t nseg = (nblk + LS_SEG - 1) / LS_SEG;
   uint32_t *segsum = W.blkcnt + BH_NLEVELS * nblk;

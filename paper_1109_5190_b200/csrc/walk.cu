@@ -57,7 +57,7 @@ namespace bh {
 #define BH_FOLD_TRIPS 16
 #endif
 #ifndef BH_WALK_MINB2
-#define BH_WALK_MINB2 8  // NP = 2 (4 targets per lane): 64 registers
+#define BH_WALK_MINB2 7  // NP = 2 (4 targets per lane): 72 registers, no spill in the loop (8 blocks: 64, cfg4 +4.5%)
 #endif
 template <int FM> struct FoldType { typedef float T; };
 template <> struct FoldType<2> { typedef double T; };
@@ -90,6 +90,23 @@ __device__ __forceinline__ void mac_one(uint32_t cc, float d2, float tacc, float
         : "+r"(res), "+r"(cnt), "+f"(f)
         : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
   }
+}
+
+// The same decision without a predicate left alive: res is updated in place
+// and the accept flag comes back as a float (1 or 0) that masks the force and
+// is summed as the count on the FMA pipe (packed, per pair).  Used where the
+// unmasked force is finite for every record (eps > 0 and no NaN distance:
+// the kernels without the containment test), so 0 x f = 0.
+__device__ __forceinline__ void mac_accf(uint32_t cc, float d2, float tacc, float trej, uint32_t skip, uint32_t dropw,
+                                         uint32_t &res, float &accf) {
+  asm("{\n\t.reg .pred pa, pc, pq;\n\t"
+      "setp.ge.u32 pa, %2, %0;\n\t"
+      "setp.gt.and.f32 pc, %3, %4, pa;\n\t"
+      "setp.ge.and.f32 pq, %3, %5, pa;\n\t"
+      "@pq selp.b32 %0, %6, %7, pc;\n\t"
+      "selp.f32 %1, 0f3F800000, 0f00000000, pc;\n\t}"
+      : "+r"(res), "=f"(accf)
+      : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
 }
 
 // STATS: also count the opened MAC tests (the flop model of bench.py).
@@ -144,37 +161,38 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
   const bool gin = gidx < ngroups;
   const int64_t grp = gin ? (P.group_list ? (int64_t)P.group_list[gidx] : gidx) : 0;
   const int64_t tbase = grp * GT + gl;
-  Target T[TPL];
-  bool v[TPL], own[TPL];
-  bool anyv = false;
-#pragma unroll
-  for (int k = 0; k < TPL; k++) {
-    const int64_t t = tbase + (int64_t)k * GL;
-    v[k] = gin && t < P.n_targets;
-    anyv |= v[k];
-    if (v[k]) T[k] = load_target(P, t);
-    else { T[k].p = 0; T[k].Li = 0; T[k].s = 0; T[k].me = make_float4(0.f, 0.f, 0.f, 0.f); }
-    own[k] = v[k] && (!P.own_check || (T[k].s >= P.own_lo && T[k].s < P.own_hi));
-  }
+  // the targets' positions (and, with CONT, own records) for the loop; the
+  // rest of a target is re-read after the loop (not kept live across it)
   uint32_t res[TPL], cnt[TPL], nop[TPL];
+  F2 CNT[NP];  // !CONT: per-pair fp32 accept counts, flushed into cnt every BH_FOLD_TRIPS trips
   float ax[TPL], ay[TPL], az[TPL];
-#pragma unroll
-  for (int k = 0; k < TPL; k++) {
-    res[k] = v[k] ? 0u : 0xffffffffu;
-    cnt[k] = 0;
-    nop[k] = 0;
-    ax[k] = ay[k] = az[k] = 0.f;
-  }
   F2 X[NP], Y[NP], Z[NP];
   uint32_t Li[TPL];
+  bool anyv = false;
+  {
+    Target T[TPL];
+    bool v[TPL];
 #pragma unroll
-  for (int j = 0; j < NP; j++) {
-    X[j] = pk2(T[2 * j].me.x, T[2 * j + 1].me.x);
-    Y[j] = pk2(T[2 * j].me.y, T[2 * j + 1].me.y);
-    Z[j] = pk2(T[2 * j].me.z, T[2 * j + 1].me.z);
+    for (int k = 0; k < TPL; k++) {
+      const int64_t t = tbase + (int64_t)k * GL;
+      v[k] = gin && t < P.n_targets;
+      anyv |= v[k];
+      if (v[k]) T[k] = load_target(P, t);
+      else { T[k].p = 0; T[k].Li = 0; T[k].s = 0; T[k].me = make_float4(0.f, 0.f, 0.f, 0.f); }
+      res[k] = v[k] ? 0u : 0xffffffffu;
+      cnt[k] = 0;
+      nop[k] = 0;
+      ax[k] = ay[k] = az[k] = 0.f;
+      Li[k] = T[k].Li;
+    }
+#pragma unroll
+    for (int j = 0; j < NP; j++) {
+      CNT[j] = pk2(0.f, 0.f);
+      X[j] = pk2(T[2 * j].me.x, T[2 * j + 1].me.x);
+      Y[j] = pk2(T[2 * j].me.y, T[2 * j + 1].me.y);
+      Z[j] = pk2(T[2 * j].me.z, T[2 * j + 1].me.z);
+    }
   }
-#pragma unroll
-  for (int k = 0; k < TPL; k++) Li[k] = T[k].Li;
   const F2 E2 = pk2(P.eps2, P.eps2);
   const bool gvalid = (__ballot_sync(full, anyv) & gmask) != 0u;
   const Rec *__restrict__ rec = P.rec;
@@ -187,6 +205,8 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
   // FM 1 / 2: the outer sums in registers; FM 3: in shared memory, [3 TPL][BLOCK]
   FoldT ox[FM == 1 || FM == 2 ? TPL : 1], oy[FM == 1 || FM == 2 ? TPL : 1], oz[FM == 1 || FM == 2 ? TPL : 1];
   __shared__ float s_out[FM == 3 ? 3 * TPL : 1][FM == 3 ? BH_WALK_BLOCK : 1];
+  // FM 3 also keeps the flushed integer counts in shared memory (no registers)
+  __shared__ uint32_t s_cnt[FM == 3 ? TPL : 1][FM == 3 ? BH_WALK_BLOCK : 1];
   if constexpr (FM == 1 || FM == 2) {
 #pragma unroll
     for (int k = 0; k < TPL; k++) ox[k] = oy[k] = oz[k] = (FoldT)0;
@@ -194,6 +214,8 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
   if constexpr (FM == 3) {
 #pragma unroll
     for (int k = 0; k < 3 * TPL; k++) s_out[k][threadIdx.x] = 0.f;
+#pragma unroll
+    for (int k = 0; k < TPL; k++) s_cnt[k][threadIdx.x] = 0u;
   }
   uint32_t trip = 0;
   if (__any_sync(full, c < Wn)) for (;;) {
@@ -245,9 +267,26 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
           qA = cA ? qnan : d2A;
           qB = cB ? qnan : d2B;
         }
-        mac_one<QUAD>(cc, qA, tacc, trej, skip, dropw, res[ka], cnt[ka], fA, g1A, g2A);
-        mac_one<QUAD>(cc, qB, tacc, trej, skip, dropw, res[kb], cnt[kb], fB, g1B, g2B);
-        const F2 FF = pk2(fA, fB);
+        F2 FF;
+        if (CONT) {
+          mac_one<QUAD>(cc, qA, tacc, trej, skip, dropw, res[ka], cnt[ka], fA, g1A, g2A);
+          mac_one<QUAD>(cc, qB, tacc, trej, skip, dropw, res[kb], cnt[kb], fB, g1B, g2B);
+          FF = pk2(fA, fB);
+        } else {
+          float accA, accB;
+          mac_accf(cc, qA, tacc, trej, skip, dropw, res[ka], accA);
+          mac_accf(cc, qB, tacc, trej, skip, dropw, res[kb], accB);
+          const F2 ACC = pk2(accA, accB);
+          FF = mul2(pk2(fA, fB), ACC);
+          CNT[j] = add2(CNT[j], ACC);
+          if (QUAD) {
+            float ta, tb;
+            up2(mul2(pk2(g1A, g1B), ACC), ta, tb);
+            g1A = ta; g1B = tb;
+            up2(mul2(pk2(g2A, g2B), ACC), ta, tb);
+            g2A = ta; g2B = tb;
+          }
+        }
         // packed accumulate on (a, b) register pairs (this form avoids ptxas moves)
         asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
             : "+f"(ax[ka]), "+f"(ax[kb]) : "l"(FF.v), "l"(DX.v));
@@ -283,9 +322,24 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
     }
     const bool live = c < Wn;
     git += live ? 1u : 0u;
-    if constexpr (FM != 0) {
-      if (++trip == BH_FOLD_TRIPS) {  // warp-uniform
-        trip = 0;
+    if (++trip == BH_FOLD_TRIPS) {  // warp-uniform
+      trip = 0;
+      if (!CONT) {  // the fp32 counts (<= 3 x BH_FOLD_TRIPS each) into the integer ones
+#pragma unroll
+        for (int j = 0; j < NP; j++) {
+          float ca, cb;
+          up2(CNT[j], ca, cb);
+          if constexpr (FM == 3) {
+            s_cnt[2 * j][threadIdx.x] += (uint32_t)ca;
+            s_cnt[2 * j + 1][threadIdx.x] += (uint32_t)cb;
+          } else {
+            cnt[2 * j] += (uint32_t)ca;
+            cnt[2 * j + 1] += (uint32_t)cb;
+          }
+          CNT[j] = pk2(0.f, 0.f);
+        }
+      }
+      if constexpr (FM != 0) {
 #pragma unroll
         for (int k = 0; k < TPL; k++) {
           if constexpr (FM == 3) {
@@ -302,6 +356,30 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
       }
     }
     if (!__any_sync(full, live)) break;
+  }
+  asm volatile("" ::: "memory");  // re-read the targets below rather than keep them live in the loop
+  Target T[TPL];
+  bool v[TPL], own[TPL];
+#pragma unroll
+  for (int k = 0; k < TPL; k++) {
+    const int64_t t = tbase + (int64_t)k * GL;
+    v[k] = gin && t < P.n_targets;
+    if (v[k]) T[k] = load_target(P, t);
+    else { T[k].p = 0; T[k].Li = 0; T[k].s = 0; T[k].me = make_float4(0.f, 0.f, 0.f, 0.f); }
+    own[k] = v[k] && (!P.own_check || (T[k].s >= P.own_lo && T[k].s < P.own_hi));
+  }
+  if (!CONT) {
+#pragma unroll
+    for (int j = 0; j < NP; j++) {
+      float ca, cb;
+      up2(CNT[j], ca, cb);
+      cnt[2 * j] += (uint32_t)ca;
+      cnt[2 * j + 1] += (uint32_t)cb;
+      if constexpr (FM == 3) {
+        cnt[2 * j] += s_cnt[2 * j][threadIdx.x];
+        cnt[2 * j + 1] += s_cnt[2 * j + 1][threadIdx.x];
+      }
+    }
   }
   double dax[TPL], day[TPL], daz[TPL];
 #pragma unroll

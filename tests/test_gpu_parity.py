@@ -215,6 +215,38 @@ def test_buckets_duplicates_coincident(BH):
     assert np.all(cnt == 999)
 
 
+@pytest.mark.parametrize("k", [40, 3000, 9000])
+def test_long_equal_key_runs(BH, k):
+    """Equal-key runs longer than 32 go to k_long_runs (bitonic tiles of 4096,
+    then pairwise merges by rank): k particles coincident with one of 2000
+    others, the coincident ones scattered through the user order and moved
+    onto the cluster point only after a step (so the run arrives in storage
+    order, not user order).  Keys / permutation / topology bit-exact against
+    the oracle (ties by user index, reading L13) at create and at the next
+    build, counts exact, forces within 1e-4."""
+    rng = np.random.default_rng(k)
+    n = 2000 + k
+    pos = rng.random((n, 3)).astype(np.float32)
+    m = (rng.random(n) + 0.5).astype(np.float32)
+    idx = rng.permutation(n)[:k]
+    pos[idx] = pos[idx[0]]  # one cluster of k coincident particles, scattered in user order
+    prm = dict(theta=0.6, eps=1e-2, G=1.0, dt=1e-3)
+    bh = BH(m, pos, None, **prm)
+    bh.build_tree()
+    o = _oracle(m, pos, None, prm)
+    check_step0(bh, o, n)
+    # the cluster re-forms from particles whose storage order is not their
+    # user order: swap the cluster with particles elsewhere and rebuild
+    pos2 = pos.copy()
+    other = np.setdiff1d(np.arange(n), idx)[: k // 2]
+    pos2[other] = pos[idx[0]]
+    pos2[idx[: k // 2]] = rng.random((k // 2, 3)).astype(np.float32)
+    bh.set_state(m, pos2, None)
+    bh.build_tree()
+    o2 = _oracle(m, pos2, None, prm)
+    check_step0(bh, o2, n)
+
+
 def test_faces_and_theta0_direct(BH):
     rng = np.random.default_rng(2)
     pos = (rng.integers(0, 5, size=(2000, 3)) * 0.25).astype(np.float32) + rng.random((2000, 3)).astype(np.float32) * 1e-3

@@ -95,7 +95,7 @@ def main():
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--command", default="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline")
-    ap.add_argument("--exclude", default="k_walk<32, 1>;k_vel4to3;k_relabel;k_pack;k_iota",
+    ap.add_argument("--exclude", default="k_walk<*, 1>;k_vel4to3;k_relabel;k_pack;k_iota",
                     help="semicolon-separated kernels launched outside the timed steps (shares also shown without them)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
@@ -108,7 +108,11 @@ def main():
         T = sum(tot.values())
         md += ["## Launch list (`--metrics gpu__time_duration.sum`, cold-cache and serialised: compare shares)", "",
                "| kernel | launches | total ms | share |", "|---|---|---|---|"]
-        excl = [x.strip() for x in a.exclude.split(";") if x.strip()]
+        import fnmatch
+
+        pats = [x.strip() for x in a.exclude.split(";") if x.strip()]
+        # (the stats walk: the k_walk instance whose last template argument, STATS, is 1)
+        excl = sorted({k for k in tot for pt in pats if fnmatch.fnmatchcase(k, pt)})
         Ts = sum(v for k, v in tot.items() if k not in excl)
         md[-2] = md[-2].replace("| share |", "| share | share of the step kernels |")
         md[-1] = "|---|---|---|---|---|"

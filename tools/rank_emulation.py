@@ -1,0 +1,73 @@
+"""Per-rank critical path of the multi-GPU step, emulated on one GPU
+(DESIGN.md §8): rank r of P as its own context (world = P,
+rank = r, no NCCL communicator), timed phase by phase with CUDA events over
+steps that run exactly what a rank runs (the full build -- every rank repeats
+it -- and the walk + leapfrog of the P = 1 groups holding its particles); the
+exchange is modelled from its bytes ((P-1)/P x 16 B x N received per GPU at
+the measured 770 GB/s peer bandwidth of B200_PROFILING.md).  Strong-scaling
+efficiency = T1 / (P x max over ranks of the rank's step).
+
+    python tools/rank_emulation.py [--config cfg5] [--ranks 2,4,8] [--steps 3]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import bhgen  # noqa: E402
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+def phases(bh, steps):
+    bh.set_profiling(True)
+    for _ in range(steps):
+        bh.step(1)
+    bh.sync()
+    pr = bh.get_profile()
+    bh.set_profiling(False)
+    return {k: v / steps for k, v in pr["ms"].items()}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--ranks", default="2,4,8")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
+    a = ap.parse_args()
+    from paper_1109_5190_b200 import BarnesHut
+
+    cfg = bhgen.CONFIGS[a.config]
+    m, p, v = bhgen.generate(cfg)
+    prm = bhgen.params(cfg)
+    one = BarnesHut(m, p, v, **prm)
+    one.step(a.warmup)
+    one.sync()
+    ph1 = phases(one, a.steps)
+    one.close()
+    t1 = sum(ph1.values())
+    print(json.dumps({"config": cfg.name, "P": 1, "phases_ms": ph1, "step_ms": t1}), flush=True)
+    for P in [int(x) for x in a.ranks.split(",")]:
+        worst, per = 0.0, []
+        for r in range(P):
+            bh = BarnesHut(m, p, v, rank=r, world=P, nccl_comm=None, **prm)
+            bh.step(a.warmup)
+            bh.sync()
+            ph = phases(bh, a.steps)
+            bh.close()
+            t = sum(ph.values())
+            per.append({"rank": r, "build_ms": ph["bbox"] + ph["keys_sort"] + ph["tree"] + ph["moments"],
+                        "walk_ms": ph["walk"], "step_ms": t})
+            worst = max(worst, t)
+        x_ms = (P - 1) / P * 16.0 * cfg.n / (NVLINK_GBS * 1e9) * 1e3
+        tp = worst + x_ms
+        print(json.dumps({"config": cfg.name, "P": P, "ranks": per, "max_rank_step_ms": worst,
+                          "exchange_model_ms": x_ms, "step_ms_model": tp, "efficiency_model": t1 / (P * tp)}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
