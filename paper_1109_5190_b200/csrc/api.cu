@@ -434,13 +434,16 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   memset(&a, 0, sizeof a);
   a.n = n;
   a.buf = ctx->sort_buf;
-  // walk_group 0 = automatic: 4-target groups (2 lanes x 2 targets, code 68)
-  // unless the walks are long (theta < 0.6 on n >= 2^22: ~2000 interactions
-  // per target), where 8-target groups of 2 lanes x 4 targets (code 69) halve
-  // the record bytes per target-visit (measured on the BASELINE configs,
-  // DESIGN.md §5)
-  a.group = ctx->p.walk_group != 0 ? ctx->p.walk_group
-                                   : ((ctx->p.theta < 0.6 && n >= ((int64_t)1 << 22)) ? 69 : 68);
+  // walk_group 0 = automatic (measured on the BASELINE configs):
+  // 4 targets per lane from 2^19 particles (half the record bytes per
+  // target-visit) -- 8-target groups of 2 lanes (code 69) for long walks
+  // (theta < 0.6: ~2000 interactions per target, cfg4) and up to 2^22 (cfg3),
+  // one lane's own 4 targets (code 70) for shorter walks on n >= 2^22 (cfg5);
+  // below 2^19 (launch-bound sizes) 2 lanes x 2 targets (code 68)
+  const int64_t nn = n;
+  const int auto_group = nn >= ((int64_t)1 << 22) ? (ctx->p.theta < 0.6 ? 69 : 70)
+                         : nn >= ((int64_t)1 << 19) ? 69 : 68;
+  a.group = ctx->p.walk_group != 0 ? ctx->p.walk_group : auto_group;
   a.stats = ctx->walk_stats;
   a.num_sms = ctx->num_sms;
   // containment test elision (see walk.cu): a cell holding the target has

@@ -203,7 +203,12 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
   const int ll = (a > b ? a : b) + 1;  // leaf level
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-  if (threadIdx.x < BH_NLEVELS) s_off[threadIdx.x] = st->lvl_offset[threadIdx.x];
+  __shared__ uint32_t s_base[BH_NLEVELS];  // level-l items of the earlier particle blocks (block-uniform)
+  if (threadIdx.x < BH_NLEVELS) {
+    const int l = threadIdx.x;
+    s_off[l] = st->lvl_offset[l];
+    s_base[l] = blkoff[l * nblk + blockIdx.x] + segoff[l * nseg + blockIdx.x / LS_SEG];
+  }
   __syncthreads();
   // in-block exclusive item ranks per level, over the levels this warp needs
   // (a+1 .. leaf level + 1: the items and their clo)
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(256) k_emit(const unsigned long long *__restri
   // items with first particle < p), l <= 22; 0 past the last level
   auto rank = [&](int l) -> uint32_t {
     if (l >= BH_NLEVELS) return 0u;
-    return blkoff[l * nblk + blockIdx.x] + segoff[l * nseg + blockIdx.x / LS_SEG] + s_pre[l][threadIdx.x] + s_w[l][w];
+    return s_base[l] + s_pre[l][threadIdx.x] + s_w[l][w];
   };
   const uint32_t base = nstart[p];
   uint32_t rk = rank(a + 1);

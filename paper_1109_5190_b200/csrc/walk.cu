@@ -314,7 +314,9 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
 #pragma unroll
       for (int k = 1; k < TPL; k++) rmin = min(rmin, res[k]);
       const bool opn = rmin <= cc;
-      if (GL == 32) {
+      if (GL == 1) {  // a lane's own group: no vote
+        c = opn ? cc + 1u : skip;
+      } else if (GL == 32) {
         c = __any_sync(full, opn) ? cc + 1u : skip;
       } else {
         c = (__ballot_sync(full, opn) & gmask2) ? cc + 1u : skip;

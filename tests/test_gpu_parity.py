@@ -292,9 +292,10 @@ def test_errors(BH):
     assert e.value.code == -3
 
 
-@pytest.mark.parametrize("cfg,group", [(c, g) for c in ("cfg2", "cfg3") for g in (66, 67, 68)])
+@pytest.mark.parametrize("cfg,group", [(c, g) for c in ("cfg2", "cfg3") for g in (66, 67, 68, 69, 70)])
 def test_walk_group_sizes(BH, cfg, group):
-    """The traversal-sharing group size (8 / 4 / 2 lanes) never changes a MAC
+    """The traversal-sharing group shape (8 / 4 / 2 lanes x 2 targets, 2 / 1
+    lanes x 4 targets) never changes a MAC
     decision: interaction counts integer-equal to the oracle's; a target's fp32
     block sums follow its group's walk, so forces agree to rounding (and with
     the oracle within 1e-4).  cfg2: theta = 0.5 (containment test elided);
@@ -315,7 +316,8 @@ def test_walk_group_sizes(BH, cfg, group):
     assert relerr(got, oacc).max() < TOL
 
 
-@pytest.mark.parametrize("cfg,group,variant", [("cfg3", 68, ""), ("cfg3", 67, ""), ("cfg3", 66, ""),
+@pytest.mark.parametrize("cfg,group,variant", [("cfg3", 68, ""), ("cfg3", 67, ""), ("cfg3", 66, ""), ("cfg3", 69, ""),
+                                               ("cfg3", 70, ""),
                                                ("cfg5", 68, ""), ("cfg3", 68, "massless"),
                                                ("cfg3", 68, "scaled")])
 def test_containment_fold_vs_test(BH, cfg, group, variant, monkeypatch):
@@ -360,12 +362,14 @@ def test_containment_fold_vs_test(BH, cfg, group, variant, monkeypatch):
         assert relerr(fa, oacc).max() < TOL
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_rank_emulation_bitwise(BH, world):
-    """Multi-GPU path emulated on one GPU (no NCCL): each rank's walk over its
-    owned Morton range gives bitwise the P = 1 forces and one-step positions."""
+@pytest.mark.parametrize("world,group", [(2, 0), (3, 0), (3, 69), (2, 70)])
+def test_rank_emulation_bitwise(BH, world, group):
+    """Multi-GPU path emulated on one GPU (no NCCL): each rank walks the P = 1
+    groups that hold its particles, so its forces and one-step positions are
+    bitwise the P = 1 ones (every group shape: the fp32 block sums follow the
+    group's walk)."""
     m, p, v = bhgen.generate("cfg2", n=30000)
-    prm = bhgen.params("cfg2")
+    prm = dict(bhgen.params("cfg2"), walk_group=group)
     one = BH(m, p, v, **prm)
     one.build_tree()
     ref = one.compute_forces()
