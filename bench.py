@@ -184,11 +184,13 @@ def reference_arm(args):
     return 0
 
 
-def walk_kernel_name(cfg, walk_group):
+def walk_kernel_name(cfg, walk_group, multipole=1):
     """The k_walk instance bh_step runs (api.cu's automatic choice for walk_group 0)."""
     shapes = {66: (8, 2), 67: (4, 2), 68: (2, 2), 69: (2, 4), 70: (1, 4)}
     g = walk_group
-    if g == 0:
+    if g == 0 and multipole == 2:
+        g = 67 if cfg.theta < 0.6 and cfg.n >= (1 << 22) else 68
+    elif g == 0:
         g = (69 if cfg.theta < 0.6 else 70) if cfg.n >= (1 << 22) else 69 if cfg.n >= (1 << 19) else 68
     lanes, tpl = shapes[g]
     return f"k_walk<{lanes},{tpl // 2}> (walk_group {g}): {lanes * tpl}-target groups, {lanes} lanes x {tpl} targets"
@@ -385,7 +387,7 @@ def ours_arm(args):
             "config": dict(workload_config(cfg, m, p, v), parallelism=f"morton-range x{world}",
                            multipole=args.multipole,
                            walk_group=args.walk_group,
-                           walk_kernel=walk_kernel_name(cfg, args.walk_group)),
+                           walk_kernel=walk_kernel_name(cfg, args.walk_group, args.multipole)),
             "particles_per_s": particles_per_s,
             "interactions_per_step": inter / args.steps,
             "fp32_peak_frac": achieved_tf / peak,

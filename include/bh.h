@@ -80,11 +80,12 @@ typedef struct {
                               n <= 199,728 and typical inputs above that)              */
     int walk_group;     /* force-walk group shape: 0 = automatic (code 68 below 2^19 particles;
                            69 up to 2^22 and for theta < 0.6 above; 70 for theta >= 0.6 from
-                           2^22); 66 / 67 / 68 = 8 / 4 / 2 lanes x 2 targets share one
-                           traversal, 69 / 70 = 2 / 1 lanes x 4 targets.  Interaction counts
-                           never depend on it; the fp32 block sums of a target follow its
-                           group's walk, so forces agree to rounding across codes and bitwise
-                           for one code at any rank count                                    */
+                           2^22; with multipole = 2: 67 for theta < 0.6 from 2^22, else 68);
+                           66 / 67 / 68 = 8 / 4 / 2 lanes x 2 targets share one traversal,
+                           69 / 70 = 2 / 1 lanes x 4 targets.  Interaction counts never depend
+                           on it; the fp32 block sums of a target follow its group's walk, so
+                           forces agree to rounding across codes and bitwise for one code at
+                           any rank count                                                    */
     int multipole;      /* cell expansion: 0 or 1 = monopole (the paper's method); 2 = monopole
                            + traceless quadrupole about the cell's centre of mass (the paper's
                            future work; reading L25 of DESIGN.md §3).  The MAC

@@ -440,8 +440,12 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   // (theta < 0.6: ~2000 interactions per target, cfg4) and up to 2^22 (cfg3),
   // one lane's own 4 targets (code 70) for shorter walks on n >= 2^22 (cfg5);
   // below 2^19 (launch-bound sizes) 2 lanes x 2 targets (code 68)
+  // (multipole = 2 keeps 2 targets per lane: its quadrupole terms fill the
+  // registers -- 4 per lane measured 117 vs 95 ms on cfg4)
   const int64_t nn = n;
-  const int auto_group = nn >= ((int64_t)1 << 22) ? (ctx->p.theta < 0.6 ? 69 : 70)
+  const bool quad = ctx->p.multipole == 2;
+  const int auto_group = quad ? ((ctx->p.theta < 0.6 && nn >= ((int64_t)1 << 22)) ? 67 : 68)
+                         : nn >= ((int64_t)1 << 22) ? (ctx->p.theta < 0.6 ? 69 : 70)
                          : nn >= ((int64_t)1 << 19) ? 69 : 68;
   a.group = ctx->p.walk_group != 0 ? ctx->p.walk_group : auto_group;
   a.stats = ctx->walk_stats;
