@@ -219,13 +219,14 @@ typedef struct {
     int64_t opens;          /* last walk: MAC tests that opened a node             */
     int64_t interactions_cum; /* all walks since bh_create                        */
     int64_t opens_cum;
-    int64_t lane_iters;     /* reserved (0)                                              */
+    int64_t record_visits;  /* last stats walk (bh_set_walk_stats): record loads, per lane */
     int64_t redo_targets;   /* last walk: targets whose fp32 MAC test was inconclusive,
                                continued with the exact fp64 test (k_walk_resume)        */
     int64_t near_sorted;    /* last build: 1 if the sort took the near-sorted path (keys
                                in the previous build's order, out-of-order keys sorted
                                apart and merged), 0 if the full radix sort ran           */
     int64_t sort_bad_keys;  /* last build, near-sorted path: keys out of local order     */
+    int64_t leaf_visits;    /* last stats walk: the record loads of particle records     */
 } bh_stats;
 bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out);
 

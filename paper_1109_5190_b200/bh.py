@@ -58,10 +58,11 @@ class BhStats(C.Structure):
         ("opens", C.c_int64),
         ("interactions_cum", C.c_int64),
         ("opens_cum", C.c_int64),
-        ("lane_iters", C.c_int64),
+        ("record_visits", C.c_int64),
         ("redo_targets", C.c_int64),
         ("near_sorted", C.c_int64),
         ("sort_bad_keys", C.c_int64),
+        ("leaf_visits", C.c_int64),
     ]
 
 

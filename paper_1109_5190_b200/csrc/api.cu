@@ -1241,7 +1241,8 @@ bh_status bh_get_stats(bh_ctx *ctx, bh_stats *out) {
   out->interactions = (int64_t)ctx->hstatus->interactions;
   out->mac_fallbacks = (int64_t)ctx->hstatus->fallbacks;
   out->opens = (int64_t)ctx->hstatus->opens;
-  out->lane_iters = (int64_t)ctx->hstatus->iters;
+  out->record_visits = (int64_t)ctx->hstatus->iters;
+  out->leaf_visits = (int64_t)ctx->hstatus->reserved0;
   out->redo_targets = (int64_t)ctx->hstatus->n_redo;
   out->near_sorted = ctx->hstatus->near_ok ? 1 : 0;
   out->sort_bad_keys = ctx->hstatus->n_bad;

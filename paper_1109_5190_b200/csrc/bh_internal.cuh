@@ -55,9 +55,9 @@ struct DevStatus {
   unsigned long long interactions;   // last walk
   unsigned long long fallbacks;      // last walk: fp64 MAC re-evaluations
   unsigned long long opens;          // last walk: MAC tests that opened a node (incl. self leaf)
-  unsigned long long iters;          // last walk: group-loop iterations summed over lanes
+  unsigned long long iters;          // last stats walk: record loads summed over lanes
   unsigned long long n_redo;         // last walk: targets re-walked with the exact fp64 MAC
-  unsigned long long reserved0;
+  unsigned long long reserved0;      // last stats walk: the record loads of particle records
   uint32_t n_own_groups;             // world > 1: walk groups holding an own particle (walk.cu)
   uint32_t n_long_runs;              // equal-key runs longer than TIE_SHORT queued for k_long_runs (sort.cu)
   uint32_t near_ok;     // this build's sort came from the near-sorted path (sort.cu)

@@ -86,7 +86,7 @@ struct ContFold {
 // one internal node of level `level` at item t (record c, children [lo, hi) of the next level)
 template <bool QUAD, bool FOLD>
 __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, uint32_t lo, uint32_t hi, uint32_t off,
-                                             uint32_t off1, double Ld, double theta,
+                                             uint32_t off1, double r_lvl, double theta,
                                              const uint32_t *__restrict__ item_rec, uint32_t *__restrict__ lvl_skip,
                                              double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
                                              double *__restrict__ lvl_q,
@@ -119,7 +119,16 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
   }
   lvl_mom[off + t] = make_double4(M, X, Y, Z);
   lvl_skip[off + t] = skip;
-  const double cx = __ddiv_rn(X, M), cy = __ddiv_rn(Y, M), cz = __ddiv_rn(Z, M);
+  // com = MX / M: the exact quotients where the quadrupoles need them (they are
+  // compared bit for bit with the oracle's); else one reciprocal (<= 1.5 ulp
+  // of fp64 off, far inside the fp32 filter's com-rounding term)
+  double cx, cy, cz;
+  if (QUAD) {
+    cx = __ddiv_rn(X, M); cy = __ddiv_rn(Y, M); cz = __ddiv_rn(Z, M);
+  } else {
+    const double iM = 1.0 / M;
+    cx = X * iM; cy = Y * iM; cz = Z * iM;
+  }
   // a massless node has no com (0/0, as in the oracle): its record gets a finite
   // dummy point and thresholds that always open it, so nothing NaN reaches the
   // walk's branch-free arithmetic (0 x NaN)
@@ -137,15 +146,15 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
         // fma per axis, no cancellation loss), then fp32.  Error budget of d
         // (relative, u = 2^-24): 3 conversions to fp32 (3u, on the squares 6u),
         // the sum of squares (3u), rsqrtf (<= 2 ulp), q2 * rsqrt (u), the
-        // conversion of M_j and its reciprocal (2u), the last multiply (u):
-        // ~17u = 1.0e-6, covered by the factor (1 + 1.5e-6) below.
+        // conversion of M_j (u) and its approximate reciprocal (<= 2 ulp), the
+        // last multiply (u): ~18u = 1.1e-6, covered by the factor (1 + 1.5e-6).
         // An overflow of the fp32 difference (large masses: q2 = +inf, rsqrt 0,
         // inf * 0 = NaN) or of d takes the fp64 route below instead -- a NaN
         // must never reach the max over children.
         const float e0 = (float)fma(mj.x, cx, -mj.y), e1 = (float)fma(mj.x, cy, -mj.z),
                     e2 = (float)fma(mj.x, cz, -mj.w);
         const float q2 = fmaf(e2, e2, fmaf(e1, e1, e0 * e0));
-        const float d = q2 > 0.f ? q2 * rsqrtf(q2) * __frcp_rn((float)mj.x) : 0.f;
+        const float d = q2 > 0.f ? q2 * rsqrtf(q2) * __fdividef(1.0f, (float)mj.x) : 0.f;
         if (d < INFINITY) return (double)d * (1.0 + 1.5e-6) + (double)rj;
       }
       double px, py, pz;
@@ -210,22 +219,26 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     }
   }
   float tacc, trej;
+  // the filter's constants: u = 2^-24; 1 / (1 -+ a) as products (their
+  // rounding, a few fp64 ulp, sits inside the 4e-15 slack)
+  constexpr double u = 5.9604644775390625e-08;
+  constexpr double a = 1.5 * u, g = 4.5 * u, delta = 1e-12;
+  constexpr double i1ma = 1.0 / (1.0 - a), i1pa = 1.0 / (1.0 + a);
+  double C = 0.0;
   if (!(theta > 0.0) || massless) {
     tacc = INFINITY;
     trej = INFINITY;
   } else {
-    const double u = 5.9604644775390625e-08;  // 2^-24
-    const double s = ldexp(Ld, -level);
-    const double r = s / theta;
-    const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
+    const double r = r_lvl;  // s_l / theta of this level (the kernel's)
+    C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
     // first-order bounds (u: com rounding |c32 - c64| <= u(1+u)|c32|, one
     // rounding of the subtraction, <= 3 roundings in the fp32 sum of squares)
     // with a safety factor 1.5 on every term
-    const double a = 1.5 * u, b = 1.5 * u * C, g = 4.5 * u, delta = 1e-12;
-    const double A = (r * (1.0 + delta) + b) / (1.0 - a);
-    tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15));
-    const double B = (r * (1.0 - delta) - b) / (1.0 + a);
-    trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 1e-15)) : -INFINITY;
+    const double b = 1.5 * u * C;
+    const double A = (r * (1.0 + delta) + b) * i1ma;
+    tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 4e-15));
+    const double B = (r * (1.0 - delta) - b) * i1pa;
+    trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 4e-15)) : -INFINITY;
     // Levels 20-21: fp32 quantisation can place a particle up to 0.19 grid
     // quanta outside its key-space cell, so there (and only there) a cell
     // containing the target could pass s/d < theta for theta < 1/sqrt(3).
@@ -234,11 +247,9 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     // re-walk, which tests containment.
     if (level >= 20) tacc = INFINITY;
     if (FOLD && level < 20) {
-      const double u = 5.9604644775390625e-08;
-      const double C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
-      const double a = 1.5 * u, b = 1.5 * u * C, g = 4.5 * u;
-      const double A = (Rn * (1.0 + 1e-12) + b) / (1.0 - a);
-      tacc = Rn == INFINITY ? INFINITY : fmaxf(tacc, round_up_f(A * A * (1.0 + g) * (1.0 + 1e-15)));
+      const double b = 1.5 * u * C;
+      const double A = (Rn * (1.0 + 1e-12) + b) * i1ma;
+      tacc = Rn == INFINITY ? INFINITY : fmaxf(tacc, round_up_f(A * A * (1.0 + g) * (1.0 + 4e-15)));
     }
   }
   Rec r;
@@ -266,7 +277,7 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
   const uint32_t off = st->lvl_offset[level];
   const uint32_t cnt1 = st->lvl_count[level + 1];
   const uint32_t off1 = st->lvl_offset[level + 1];
-  const double Ld = (double)st->L;
+  const double r_lvl = ldexp((double)st->L, -level) / theta;  // s_l / theta
   // one round trip for an item, one for its children (loads hoisted so they
   // are in flight together); the next item's loads are issued before this
   // one's children are summed
@@ -291,7 +302,7 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
     lo = lon;
     hi = hin;
     if (ecur & ITEM_LEAF) continue;  // a particle: K4 wrote its record and moments
-    moments_node<QUAD, FOLD>(level, t, ecur, locur, hicur, off, off1, Ld, theta, item_rec, lvl_skip, lvl_mom, rec,
+    moments_node<QUAD, FOLD>(level, t, ecur, locur, hicur, off, off1, r_lvl, theta, item_rec, lvl_skip, lvl_mom, rec,
                        lvl_q, qmom, qrec, cf, st);
   }
 }

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
   // the targets' positions (and, with CONT, own records) for the loop; the
   // rest of a target is re-read after the loop (not kept live across it)
   uint32_t res[TPL], cnt[TPL], nop[TPL];
+  uint32_t sv_rec = 0, sv_leaf = 0;  // STATS: record loads, of particle records
   F2 CNT[NP];  // !CONT: per-pair fp32 accept counts, flushed into cnt every BH_FOLD_TRIPS trips
   float ax[TPL], ay[TPL], az[TPL];
   F2 X[NP], Y[NP], Z[NP];
@@ -309,6 +310,8 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
       if (STATS) {
 #pragma unroll
         for (int k = 0; k < TPL; k++) nop[k] += res[k] <= cc ? 1u : 0u;
+        sv_rec += cc < Wn ? 1u : 0u;
+        sv_leaf += (cc < Wn && au.x == 0xff800000u) ? 1u : 0u;  // T_acc = -inf: a particle record
       }
       uint32_t rmin = res[0];
 #pragma unroll
@@ -422,9 +425,20 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
     atomicAdd(&P.st->interactions, wc);
     atomicAdd(&P.st->interactions_cum, wc);
   }
-  if (STATS && lane == 0 && wo) {
-    atomicAdd(&P.st->opens, wo);
-    atomicAdd(&P.st->opens_cum, wo);
+  if (STATS) {
+    unsigned long long r1 = sv_rec, r2 = sv_leaf;
+    for (int o = 16; o; o >>= 1) {
+      r1 += __shfl_xor_sync(full, r1, o);
+      r2 += __shfl_xor_sync(full, r2, o);
+    }
+    if (lane == 0) {
+      if (wo) {
+        atomicAdd(&P.st->opens, wo);
+        atomicAdd(&P.st->opens_cum, wo);
+      }
+      atomicAdd(&P.st->iters, r1);
+      atomicAdd(&P.st->reserved0, r2);
+    }
   }
 #pragma unroll
   for (int k = 0; k < TPL; k++) {

@@ -216,6 +216,8 @@ __device__ __forceinline__ void fma2_acc(F2 &acc, F2 a, F2 b) {  // acc = a * b 
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.v) : "l"(a.v), "l"(b.v));
 }
 
+// one record, one 32-byte load (measured r2: the record split into two 16-B
+// arrays -- two loads per visit -- cost cfg4 +37 %, cfg5 +43 % walk time)
 __device__ __forceinline__ void ld_rec(const Rec *p, float4 &cm, uint4 &au) {
   asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(cm.x), "=f"(cm.y), "=f"(cm.z), "=f"(cm.w), "=r"(au.x), "=r"(au.y), "=r"(au.z), "=r"(au.w)
