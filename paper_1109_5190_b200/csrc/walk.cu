@@ -493,7 +493,7 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.st = W.status;
   P.icount = W.icount;
   P.redo = W.redo;
-  P.gcost = (!a.stats && !getenv("BH_NO_GROUP_ORDER")) ? W.gcost : nullptr;
+  P.gcost = !getenv("BH_NO_GROUP_ORDER") ? W.gcost : nullptr;
   P.resume = W.resume;
   P.cap_resume = W.cap_resume;
   P.resume_stack = W.resume_stack > 0 && W.resume_stack < RESUME_STACK ? W.resume_stack : RESUME_STACK;
