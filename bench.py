@@ -235,6 +235,13 @@ def ours_arm(args):
     bh = BarnesHut(m, p, v, device=device, rank=rank, world=world, nccl_comm=comm, walk_group=args.walk_group,
                    multipole=args.multipole, **prm)
     stream = bh.stream
+    exchange_kind = "nccl_broadcast" if world > 1 else None
+    if world > 1 and args.exchange == "fused":
+        # K8 fused into K7: every rank's replica opened by CUDA IPC, the walk
+        # epilogue stores into all of them; the step's two barriers are one-word
+        # NCCL all-reduces inside the captured graph (bh_set_peers)
+        bdist.share_replicas(bh, dist)
+        exchange_kind = "fused_peer_stores"
     props = torch.cuda.get_device_properties(device)
     sms = props.multi_processor_count
 
@@ -413,11 +420,16 @@ def ours_arm(args):
             "ms_per_step_profiled_phases": sum(phase_ms.values()),
             "clocks": clocks,
             "nccl": nccl_info,
+            "exchange": exchange_kind,
             "ownership_balance": balance,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
         print(json.dumps(out), flush=True)
+    if exchange_kind == "fused_peer_stores":
+        bh.sync()
+        dist.barrier()  # no rank unmaps a replica another may still write
+        bh.set_peers(None)
     bh.close()
     if comm is not None:
         bhmod.nccl_comm_destroy(comm)
@@ -475,6 +487,9 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true", help="N > 1: keep the even Morton-range split")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: K8 as a grouped ncclBroadcast after the walk, or fused into the walk's "
+                         "epilogue (peer stores into every replica, bh_set_peers)")
     ap.add_argument("--rebalance-every", type=int, default=0,
                     help="N > 1: also re-split ownership by cost every K timed steps (0: once, after warm-up)")
     ap.add_argument("--cpu-samples", type=int, default=20000)

@@ -208,6 +208,33 @@ bh_status bh_get_pos4(bh_ctx *ctx, float *pos4, int64_t lo, int64_t hi, int wher
 bh_status bh_set_pos4(bh_ctx *ctx, const float *pos4, int64_t lo, int64_t hi, int where);
 bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel, int where);
 
+/* The fused exchange (the per-iteration global barrier
+ * of PAPER.md:441-444, §3).  K8 is folded into K7: the walk's leapfrog epilogue
+ * stores each updated own position into this rank's pos4 AND into every other
+ * rank's replica (peer memory: NVLink stores, 16 B per particle per peer), so
+ * the exchange overlaps the walk instead of following it.
+ * bh_get_pos4_ptr: the device address of this ctx's pos4 replica (float4[n],
+ *   storage order, inside the caller's workspace: same offset on every rank),
+ *   for the caller to share (same process: the pointer; other processes: a CUDA
+ *   IPC handle of the workspace, paper_1109_5190_b200.dist.share_replicas).
+ * bh_set_peers: pos4_of_rank[world] = every rank's replica as a device pointer
+ *   valid on this ctx's device (this rank's own entry is ignored); NULL turns
+ *   the fused exchange off (back to K8's grouped ncclBroadcast).  The pointers
+ *   are borrowed until the next bh_set_peers / bh_destroy; world - 1 <= 15.
+ *   Ordering: with an NCCL communicator every step runs build -> barrier (a
+ *   one-word ncclAllReduce) -> walk with peer stores -> barrier, captured in
+ *   the step graph.  Without one, the caller orders the ranks' phases with
+ *   bh_step_phase (all ranks' phase 0, then all ranks' phase 1) and a device
+ *   sync between them.  Results are bitwise those of bh_step with the
+ *   broadcast (tests/test_gpu_parity.py, tests/test_gpu_multiproc.py).  Syncs.
+ * bh_step_phase: one step in two calls; phase 0 = K0-K5 (the tree of the
+ *   current positions), phase 1 = K6-K8 (walk, leapfrog, exchange);
+ *   bh_step(ctx, 1) == phase 0 + phase 1.  BH_ERR_STATE for phase 1 without a
+ *   fresh phase 0.  Direct launches (no graph).  Asynchronous. */
+bh_status bh_get_pos4_ptr(bh_ctx *ctx, void **dev_ptr);
+bh_status bh_set_peers(bh_ctx *ctx, void *const *pos4_of_rank);
+bh_status bh_step_phase(bh_ctx *ctx, int phase);
+
 typedef struct {
     int64_t n_records;      /* walk records: tree nodes + bucket members          */
     int64_t n_internal;     /* internal nodes incl. buckets                       */

@@ -108,6 +108,9 @@ def load_library(path: str = LIB_PATH):
             "bh_get_pos4": (i32, [vp, vp, i64, i64, i32]),
             "bh_set_pos4": (i32, [vp, vp, i64, i64, i32]),
             "bh_set_partition": (i32, [vp, vp, vp, i32]),
+            "bh_get_pos4_ptr": (i32, [vp, C.POINTER(vp)]),
+            "bh_set_peers": (i32, [vp, vp]),
+            "bh_step_phase": (i32, [vp, i32]),
             "bh_get_stats": (i32, [vp, C.POINTER(BhStats)]),
             "bh_set_profiling": (i32, [vp, i32]),
             "bh_set_walk_stats": (i32, [vp, i32]),
@@ -356,6 +359,25 @@ class BarnesHut:
     def set_pos4(self, a, lo, hi):
         a = np.ascontiguousarray(a, dtype=np.float32).reshape(-1, 4)
         self._chk(self.L.bh_set_pos4(self.h, _ptr(a), int(lo), int(hi), BH_HOST))
+
+    def pos4_ptr(self) -> int:
+        """Device address of this ctx's pos4 replica (inside self.workspace)."""
+        out = C.c_void_p()
+        self._chk(self.L.bh_get_pos4_ptr(self.h, C.byref(out)))
+        return int(out.value)
+
+    def set_peers(self, pos4_of_rank):
+        """The fused exchange (bh_set_peers): every rank's pos4 replica as a device
+        address on this ctx's device (this rank's entry ignored); None = off."""
+        if pos4_of_rank is None:
+            self._chk(self.L.bh_set_peers(self.h, None))
+            return
+        arr = (C.c_void_p * len(pos4_of_rank))(*[int(x) if x else None for x in pos4_of_rank])
+        self._chk(self.L.bh_set_peers(self.h, C.cast(arr, C.c_void_p)))
+
+    def step_phase(self, phase):
+        """Half a step: 0 = build the tree (K0-K5), 1 = walk + leapfrog + exchange."""
+        self._chk(self.L.bh_step_phase(self.h, int(phase)))
 
     def set_partition(self, bounds, vel_own):
         """New ownership bounds[world + 1] and the new own slice's velocities."""

@@ -44,6 +44,8 @@ struct bh_ctx {
   int sort_buf;
   int near_sort;        // 1: try the near-sorted path each build (nearsort.cu)
   int cont_fold;        // containment folded into T_acc (com.cu): the walk skips its per-visit test
+  // fused exchange (bh_set_peers): the other ranks' pos4 replicas, written by K7
+  std::vector<float4 *> peers;
   DevStatus *hstatus;  // pinned
   cudaEvent_t status_ev;
   // bh_advance: the velocity upload runs on io_stream beside the first build
@@ -243,8 +245,12 @@ __global__ void k_load_vel(float4 *__restrict__ vel4, const uint32_t *__restrict
 
 // K7 apart (bh_advance's first step): v += a kick, x += v dt, as the walk's
 // fused epilogue does it (acc: own slice, storage order, G applied)
+struct PeerPtrs {
+  int n;
+  float4 *p[BH_MAX_PEERS];
+};
 __global__ void k_kick_drift(float4 *__restrict__ pos4, float4 *__restrict__ vel4, const float *__restrict__ acc,
-                             int64_t lo, int64_t hi, float kick, float dt) {
+                             int64_t lo, int64_t hi, float kick, float dt, const PeerPtrs peers) {
   int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= hi) return;
   const size_t o = (size_t)(s - lo);
@@ -254,7 +260,9 @@ __global__ void k_kick_drift(float4 *__restrict__ pos4, float4 *__restrict__ vel
   v.z = fmaf(acc[3 * o + 2], kick, v.z);
   vel4[o] = v;
   const float4 x = pos4[s];
-  pos4[s] = make_float4(fmaf(v.x, dt, x.x), fmaf(v.y, dt, x.y), fmaf(v.z, dt, x.z), x.w);
+  const float4 y = make_float4(fmaf(v.x, dt, x.x), fmaf(v.y, dt, x.y), fmaf(v.z, dt, x.z), x.w);
+  pos4[s] = y;
+  for (int k = 0; k < peers.n; k++) peers.p[k][s] = y;  // bh_set_peers: the fused exchange
 }
 
 // user-order outputs from storage slots [lo, hi): out[uid[s]] = src(s)
@@ -465,6 +473,8 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.own_hi = (uint32_t)ctx->own_hi;
   a.acc_out = mode == 0 ? acc_out : nullptr;
   a.user_order = user_order ? 1 : 0;
+  a.n_peers = (int)ctx->peers.size();
+  a.peer_pos4 = ctx->peers.data();
   CK(cudaMemsetAsync(&ctx->W.status->interactions, 0, 6 * sizeof(unsigned long long), s));
   // world > 1: the rank walks the P = 1 groups that hold one of its particles
   // (every target summed in the same group as at P = 1: bitwise equal results)
@@ -476,8 +486,28 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   return BH_OK;
 }
 
+// bh_set_peers with a communicator: a one-word all-reduce orders the ranks'
+// phases (every replica written before anyone builds from it; nobody writes a
+// replica its owner still reads)
+static bh_status peer_barrier(bh_ctx *ctx) {
+  if (ctx->peers.empty() || !ctx->p.nccl_comm) return BH_OK;
+  uint32_t *w = &ctx->W.status->pad[0];
+  ncclResult_t rc = ncclAllReduce(w, w, 1, ncclUint32, ncclMax, (ncclComm_t)ctx->p.nccl_comm, ctx->stream);
+  if (rc != ncclSuccess) return fail(ctx, BH_ERR_NCCL, "ncclAllReduce (barrier): %s", ncclGetErrorString(rc));
+  return BH_OK;
+}
+
 static bh_status exchange(bh_ctx *ctx) {
-  if (ctx->p.world == 1 || !ctx->p.nccl_comm) return BH_OK;
+  if (ctx->p.world == 1) return BH_OK;
+  if (!ctx->peers.empty()) {  // K8 rode on K7's stores: only the barrier is left
+    ProfPair pp;
+    prof_begin(ctx, &pp, 5);
+    bh_status st = peer_barrier(ctx);
+    if (st) return st;
+    prof_end(ctx, &pp, ctx->p.nccl_comm ? 1 : 0);
+    return BH_OK;
+  }
+  if (!ctx->p.nccl_comm) return BH_OK;
   ProfPair pp;
   prof_begin(ctx, &pp, 5);
   ncclComm_t comm = (ncclComm_t)ctx->p.nccl_comm;
@@ -731,9 +761,20 @@ static bh_status flush_vel(bh_ctx *ctx) {
   return BH_OK;
 }
 
+static bh_status enqueue_walk(bh_ctx *ctx, float kick);
 static bh_status enqueue_step(bh_ctx *ctx, float kick) {
   bh_status st = build_tree(ctx);
   if (st) return st;
+  // bh_set_peers: every rank has finished reading its replica before any K7
+  // writes into it
+  st = peer_barrier(ctx);
+  if (st) return st;
+  return enqueue_walk(ctx, kick);
+}
+
+// K6-K8 of a step on the tree just built
+static bh_status enqueue_walk(bh_ctx *ctx, float kick) {
+  bh_status st = BH_OK;
   if (ctx->vel_pending) {
     // first step of bh_advance: the walk computes forces (own slice, storage
     // order) while the velocity upload finishes, then K7 runs apart with the
@@ -743,8 +784,11 @@ static bh_status enqueue_step(bh_ctx *ctx, float kick) {
     st = flush_vel(ctx);
     if (st) return st;
     const int64_t own_n = ctx->own_hi - ctx->own_lo;
+    PeerPtrs pp;
+    pp.n = (int)ctx->peers.size();
+    for (int k = 0; k < BH_MAX_PEERS; k++) pp.p[k] = k < pp.n ? ctx->peers[k] : nullptr;
     k_kick_drift<<<blocks_for(own_n), 256, 0, ctx->stream>>>(ctx->W.pos4, ctx->W.vel4, ctx->W.accu, ctx->own_lo,
-                                                              ctx->own_hi, kick, (float)ctx->p.dt);
+                                                              ctx->own_hi, kick, (float)ctx->p.dt, pp);
     CK(cudaGetLastError());
   } else {
     st = walk(ctx, 1, kick, nullptr, false);
@@ -1195,6 +1239,57 @@ bh_status bh_get_pos4(bh_ctx *ctx, float *pos4, int64_t lo, int64_t hi, int wher
     CK(cudaMemcpyAsync(pos4, ctx->W.pos4 + lo, (size_t)(hi - lo) * 16,
                        where == BH_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
   return do_sync(ctx);
+}
+
+// ---- the fused exchange (NEXT-1, include/bh.h) -----------------------------
+bh_status bh_get_pos4_ptr(bh_ctx *ctx, void **dev_ptr) {
+  if (!ctx || !dev_ptr) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  *dev_ptr = (void *)ctx->W.pos4;
+  return BH_OK;
+}
+
+bh_status bh_set_peers(bh_ctx *ctx, void *const *pos4_of_rank) {
+  if (!ctx) return BH_ERR_ARG;
+  const int P = ctx->p.world, r = ctx->p.rank;
+  std::vector<float4 *> peers;
+  if (pos4_of_rank) {
+    if (P < 2) return fail(ctx, BH_ERR_ARG, "bh_set_peers needs world > 1");
+    if (P - 1 > BH_MAX_PEERS) return fail(ctx, BH_ERR_ARG, "world %d exceeds %d peers", P, BH_MAX_PEERS);
+    for (int q = 0; q < P; q++) {
+      if (q == r) continue;
+      if (!pos4_of_rank[q]) return fail(ctx, BH_ERR_ARG, "null replica pointer of rank %d", q);
+      if (pos4_of_rank[q] == (void *)ctx->W.pos4) return fail(ctx, BH_ERR_ARG, "rank %d's replica is this rank's", q);
+      peers.push_back((float4 *)pos4_of_rank[q]);
+    }
+  }
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  st = do_sync(ctx);
+  if (st) return st;
+  ctx->peers = peers;
+  drop_graphs(ctx);  // the replica pointers are baked into the captured steps
+  return BH_OK;
+}
+
+// one step in two calls, for callers that interleave several ranks' phases
+// (bh_step(ctx, 1) == bh_step_phase(ctx, 0) + bh_step_phase(ctx, 1))
+bh_status bh_step_phase(bh_ctx *ctx, int phase) {
+  if (!ctx || (phase != 0 && phase != 1)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  if (phase == 0) {
+    st = build_tree(ctx);
+    if (st) return st;
+    return enqueue_status(ctx);
+  }
+  if (!ctx->tree_valid) return fail(ctx, BH_ERR_STATE, "bh_step_phase(1) needs bh_step_phase(0) first");
+  if (ctx->prof) ctx->prof_calls++;
+  const float kick = (float)(ctx->steps == 0 ? 0.5 * ctx->p.dt : ctx->p.dt);
+  st = enqueue_walk(ctx, kick);
+  if (st) return st;
+  ctx->steps++;
+  ctx->tree_valid = false;
+  return enqueue_status(ctx);
 }
 
 bh_status bh_set_pos4(bh_ctx *ctx, const float *pos4, int64_t lo, int64_t hi, int where) {

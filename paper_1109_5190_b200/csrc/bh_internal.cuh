@@ -34,6 +34,7 @@
 #define BH_MAXLEVEL 21
 #define BH_NLEVELS 23  // item levels 0 .. 22 (22: bucket members)
 #define BH_NPHASE 6
+#define BH_MAX_PEERS 15  // bh_set_peers: replicas written by K7 besides the own one (world <= 16)
 
 namespace bh {
 
@@ -207,6 +208,8 @@ struct WalkArgs {
   uint32_t own_lo, own_hi;
   float *acc_out;       // mode 0: [n][3] device output (may be null)
   int user_order;       // 1: acc_out[uid[s]], 0: acc_out[s - own_lo]
+  int n_peers;          // mode 1, bh_set_peers: the other ranks' pos4 replicas K7 also writes
+  float4 *const *peer_pos4;
 };
 cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s);
 int walk_lanes(int group);

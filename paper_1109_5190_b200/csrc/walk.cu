@@ -513,6 +513,8 @@ cudaError_t launch_walk(const Workspace &W, const WalkArgs &a, cudaStream_t s) {
   P.own_hi = a.own_hi;
   P.own_check = a.own_check;
   P.num_sms = a.num_sms > 0 ? a.num_sms : 148;
+  P.n_peers = a.mode == 1 ? a.n_peers : 0;
+  for (int k = 0; k < BH_MAX_PEERS; k++) P.peer_pos4[k] = k < P.n_peers ? a.peer_pos4[k] : nullptr;
   const int GL = walk_lanes(a.group), GT = walk_tpl(a.group) * GL;
   const int64_t ng_all = (a.n + GT - 1) / GT;
   int64_t ng_max = ng_all;

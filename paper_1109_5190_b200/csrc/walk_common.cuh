@@ -81,6 +81,10 @@ struct WalkParams {
   double theta2;
   uint32_t own_lo, own_hi;
   int num_sms;
+  // fused exchange (bh_set_peers): every other rank's pos4 replica, written
+  // by K7 beside the own copy (peer memory over NVLink)
+  int n_peers;
+  float4 *peer_pos4[BH_MAX_PEERS];
 };
 
 __device__ __forceinline__ float rsqrt_fast(float x) {
@@ -153,7 +157,11 @@ __device__ __forceinline__ void finish(const WalkParams &P, const Target &T, dou
     v.y = fmaf(gy, P.kick, v.y);
     v.z = fmaf(gz, P.kick, v.z);
     P.vel4[o] = v;
-    P.pos4[T.s] = make_float4(fmaf(v.x, P.dt, T.me.x), fmaf(v.y, P.dt, T.me.y), fmaf(v.z, P.dt, T.me.z), T.me.w);
+    const float4 x = make_float4(fmaf(v.x, P.dt, T.me.x), fmaf(v.y, P.dt, T.me.y), fmaf(v.z, P.dt, T.me.z), T.me.w);
+    P.pos4[T.s] = x;
+    // K8 fused into K7 (bh_set_peers): the new position goes straight into
+    // every other rank's replica, so the exchange rides on the walk
+    for (int k = 0; k < P.n_peers; k++) P.peer_pos4[k][T.s] = x;
   }
 }
 

@@ -4,9 +4,11 @@ bootstrap through torch.distributed, and max/sum reductions over ranks.
 The data path itself is in libbh.so: every rank holds the full position array,
 builds the same tree, walks and integrates its own contiguous Morton range and
 then broadcasts that slice to every other rank (api.cu `exchange`, a grouped
-ncclBroadcast per owner).  This module only mirrors the partition rule and
-moves small host objects; it is tested with the gloo backend on CPU
-(tests/test_dist_gloo.py) because this environment has a single GPU.
+ncclBroadcast per owner) -- or, with share_replicas / bh_set_peers, stores
+each new position straight into every rank's replica from the walk epilogue.
+This module only mirrors the partition rule and moves small host objects; it
+is tested with the gloo backend on CPU (tests/test_dist_gloo.py) because this
+environment has a single GPU.
 """
 from __future__ import annotations
 
@@ -88,6 +90,33 @@ def rebalance(bh, dist, device=None):
     me = dist.get_rank()
     bh.set_partition(bounds, vels[bounds[me]:bounds[me + 1]])
     return bounds
+
+
+def share_replicas(bh, dist):
+    """Collective: the fused exchange's plumbing (bh_set_peers).  Every rank
+    exports its workspace as a CUDA IPC handle (torch.multiprocessing's
+    reduce_tensor), all-gathers the handles with pos4's offset inside the
+    workspace, opens the other ranks' workspaces (peer memory, mapped with
+    lazy peer access) and hands the library every rank's pos4 address.  The
+    opened mappings are kept on `bh` for as long as the peers are set."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    world, me = dist.get_world_size(), dist.get_rank()
+    off = bh.pos4_ptr() - bh.workspace.data_ptr()
+    fn, args = reduce_tensor(bh.workspace)
+    objs = [None] * world
+    dist.all_gather_object(objs, (fn, args, off))
+    ptrs, keep = [], []
+    for r, (f, a, o) in enumerate(objs):
+        if r == me:
+            ptrs.append(bh.pos4_ptr())
+            continue
+        t = f(*a)
+        keep.append(t)
+        ptrs.append(t.data_ptr() + o)
+    bh._peer_workspaces = keep
+    bh.set_peers(ptrs)
+    return ptrs
 
 
 def share_nccl_id(make_id, dist) -> bytes:

@@ -5,6 +5,8 @@ through bh_get_pos4 / bh_set_pos4 (no NCCL communicator: nccl_comm = NULL), and
 dist.rebalance runs on the real BarnesHut objects mid-run (equal-cost split
 from the last walk's interaction counts).  The processes never wait on each
 other inside a kernel (only host collectives), so sharing the GPU is safe.
+The fused variant shares the replicas by CUDA IPC instead (dist.share_replicas:
+the walk epilogue of each process stores into the other's pos4; NEXT-1).
 Bar: every particle's position and velocity after 4 steps bitwise equal to the
 P = 1 run, and within 1e-4 of the fp64 oracle (every
 iteration needs all particles' positions)."""
@@ -27,7 +29,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, out_q):
+def _rank(rank, world, port, out_q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch
@@ -44,11 +46,25 @@ def _rank(rank, world, port, out_q):
         bh = BarnesHut(m, p, v, device=0, rank=rank, world=world, nccl_comm=None, **prm)
         bounds = [N * r // world for r in range(world + 1)]
         moved = None
+        if fused:  # K8 fused into K7: IPC-shared replicas (bh_set_peers)
+            ptrs = bdist.share_replicas(bh, dist)
+            assert len(set(ptrs)) == world
         for k in range(STEPS):
             if k == REBALANCE_AT:
                 new = bdist.rebalance(bh, dist)  # all-gathers costs + velocities, bh_set_partition
                 moved = new != bounds
                 bounds = new
+            if fused:
+                # every rank builds from the old positions, then every rank's walk
+                # stores its new positions into all replicas; host barriers order
+                # the phases (a communicator would put them in the step's graph)
+                bh.step_phase(0)
+                bh.sync()
+                dist.barrier()
+                bh.step_phase(1)
+                bh.sync()
+                dist.barrier()
+                continue
             bh.step(1)
             # K8 over gloo: every owner's slice of pos4 (x, y, z, m) to every rank
             mine = torch.from_numpy(bh.get_pos4(bounds[rank], bounds[rank + 1]))
@@ -60,12 +76,16 @@ def _rank(rank, world, port, out_q):
         pos, vel = bh.get_state()
         st = bh.get_stats()
         out_q.put((rank, pos, vel, (int(st["own_begin"]), int(st["own_end"])), bounds, moved))
+        if fused:
+            bh.set_peers(None)
+            dist.barrier()  # nobody unmaps a replica another rank may still write
         bh.close()
     finally:
         dist.destroy_process_group()
 
 
-def test_two_processes_one_gpu_gloo_exchange_and_rebalance():
+@pytest.mark.parametrize("fused", [False, True], ids=["gloo_exchange", "fused_peer_stores"])
+def test_two_processes_one_gpu_gloo_exchange_and_rebalance(fused):
     import torch
     import torch.multiprocessing as mp
 
@@ -79,7 +99,7 @@ def test_two_processes_one_gpu_gloo_exchange_and_rebalance():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, fused)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])

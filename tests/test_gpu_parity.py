@@ -697,6 +697,64 @@ def test_multirank_steps_external_exchange_bitwise(BH, world, rebalance_at):
     assert relerr(got_pos, opos).max() < TOL
 
 
+@pytest.mark.parametrize("world,rebalance_at", [(2, None), (3, 2)])
+def test_fused_exchange_peer_stores_bitwise(BH, world, rebalance_at):
+    """K8 fused into K7 (bh_set_peers, NEXT-1): P single-GPU ranks in one
+    process, each holding the others' pos4 replicas as peer pointers; every
+    step is all ranks' bh_step_phase(0) (build), a sync, then all ranks'
+    bh_step_phase(1) (walk + leapfrog storing each new own position into every
+    replica), a sync -- no exchange call at all.  After 4 steps (an equal-cost
+    repartition in between for P = 3) every replica holds bitwise the P = 1
+    positions, the own velocities are bitwise P = 1's, and the trajectory is
+    within 1e-4 of the free-running oracle."""
+    m, p, v = bhgen.generate("cfg2", n=20000)
+    prm = bhgen.params("cfg2")
+    n = m.shape[0]
+    one = BH(m, p, v, **prm)
+    one.build_tree()
+    _, perm = one.get_keys()
+    one.step(4)
+    ref_pos, ref_vel = one.get_state()
+    from paper_1109_5190_b200 import dist as bdist
+
+    ranks = [BH(m, p, v, rank=r, world=world, **prm) for r in range(world)]
+    ptrs = [bh.pos4_ptr() for bh in ranks]
+    assert len(set(ptrs)) == world
+    for bh in ranks:
+        bh.set_peers(ptrs)
+    bounds = [n * r // world for r in range(world + 1)]
+    for k in range(4):
+        if rebalance_at is not None and k == rebalance_at:
+            costs = np.concatenate([bh.get_own()[0] for bh in ranks]).astype(np.float64)
+            vels = np.concatenate([bh.get_own()[1] for bh in ranks])
+            bounds = bdist.cost_bounds(costs, world)
+            for r, bh in enumerate(ranks):
+                bh.set_partition(bounds, vels[bounds[r]:bounds[r + 1]])
+        for bh in ranks:
+            bh.step_phase(0)
+        for bh in ranks:
+            bh.sync()
+        for bh in ranks:
+            bh.step_phase(1)
+        for bh in ranks:
+            bh.sync()
+    got_vel = np.full_like(ref_vel, np.nan)
+    for r, bh in enumerate(ranks):
+        pos, vel = bh.get_state()
+        assert np.array_equal(pos, ref_pos)  # every replica, all particles
+        own = perm[bounds[r]:bounds[r + 1]].astype(np.int64)
+        got_vel[own] = vel[own]
+    assert np.array_equal(got_vel, ref_vel)
+    with pytest.raises(Exception):
+        ranks[0].step_phase(1)  # phase 1 needs a fresh phase 0
+    for bh in ranks:
+        bh.set_peers(None)
+    o = _oracle(m, p, v, prm)
+    o.step(4)
+    opos, ovel = o.state()
+    assert relerr(ref_pos, opos).max() < TOL and relerr(got_vel, ovel).max() < TOL
+
+
 @pytest.mark.parametrize("cfg,n", [("cfg2", 30000), ("cfg3", 40000)])
 def test_quadrupole_parity(BH, cfg, n):
     """multipole = 2 (NEXT-3, reading L25): keys / tree / fp64 moments AND fp64
