@@ -53,6 +53,9 @@ namespace bh {
 #ifndef BH_FOLD_NP2
 #define BH_FOLD_NP2 3  // NP = 2 (0 / 1 / 3)
 #endif
+#ifndef BH_RSQRT_NEWTON
+#define BH_RSQRT_NEWTON 0
+#endif
 #ifndef BH_FOLD_TRIPS
 #define BH_FOLD_TRIPS 16
 #endif
@@ -238,8 +241,18 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
         // the interaction of both targets, branch-free (f zeroed for a target
         // that does not accept the record)
         float r2A, r2B;
-        up2(add2(D2, E2), r2A, r2B);
+        const F2 R2 = add2(D2, E2);
+        up2(R2, r2A, r2B);
+#if BH_RSQRT_NEWTON
+        // (accuracy experiment: one Newton step on MUFU.RSQ, y (1.5 - 0.5 r2 y^2))
+        F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
+        {
+          const F2 H = fma2(pk2(-0.5f, -0.5f), mul2(mul2(R2, INV), INV), pk2(1.5f, 1.5f));
+          INV = mul2(INV, H);
+        }
+#else
         const F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
+#endif
         float fA, fB;
         const F2 INV2 = mul2(INV, INV);
         up2(mul2(mul2(pk2(cm.w, cm.w), INV2), INV), fA, fB);
