@@ -11,7 +11,7 @@ python bench.py --config $CFG > $O/${R}_bench_${CFG}.json 2> $O/${R}_bench_${CFG
 CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > $O/${R}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${R}_launches.csv $CMD > /dev/null 2>&1
-for spec in "walk:^k_walk$:1" "resume:k_walk_resume:1" "moments:k_moments_local:1" "emit:k_emit:1" "keys_prev:k_keys_prev:1" "merge:k_near_merge:1" "split:k_near_split:1"; do
+for spec in "walk:^k_walk$:1" "resume:k_walk_resume:1" "moments:k_moments_level:33" "emit:k_emit:1" "keys_prev:k_keys_prev:1" "merge:k_near_merge:1" "split:k_near_split:1"; do
   IFS=: read key kern skip <<< "$spec"
   ncu --set full --clock-control none --import-source on -k "regex:$kern" -s $skip -c 1 -o $O/${R}_prof_$key $CMD > $O/${R}_ncu_$key.log 2>&1
 done
