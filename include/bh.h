@@ -225,7 +225,9 @@ bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel,
  *   one-word ncclAllReduce) -> walk with peer stores -> barrier, captured in
  *   the step graph.  Without one, the caller orders the ranks' phases with
  *   bh_step_phase (all ranks' phase 0, then all ranks' phase 1) and a device
- *   sync between them.  Results are bitwise those of bh_step with the
+ *   sync between them; bh_step / bh_advance then return BH_ERR_STATE (nothing
+ *   would order this rank's stores after the others' builds).  Results are
+ *   bitwise those of bh_step with the
  *   broadcast (tests/test_gpu_parity.py, tests/test_gpu_multiproc.py).  Syncs.
  * bh_step_phase: one step in two calls; phase 0 = K0-K5 (the tree of the
  *   current positions), phase 1 = K6-K8 (walk, leapfrog, exchange);

@@ -841,8 +841,14 @@ static bh_status step_graph(bh_ctx *ctx, int which, float kick, cudaGraphExec_t 
   return BH_OK;
 }
 
+// bh_set_peers without a communicator: nothing inside a step orders this rank's
+// K7 stores after the other ranks' builds, so only bh_step_phase may step
+static bool peers_unordered(const bh_ctx *ctx) { return !ctx->peers.empty() && !ctx->p.nccl_comm; }
+
 bh_status bh_step(bh_ctx *ctx, int nsteps) {
   if (!ctx || nsteps < 0) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  if (nsteps > 0 && peers_unordered(ctx))
+    return fail(ctx, BH_ERR_STATE, "bh_set_peers without an NCCL communicator: step with bh_step_phase");
   bh_status st = set_dev(ctx);
   if (st) return st;
   if (ctx->status_pending && cudaEventQuery(ctx->status_ev) == cudaSuccess) {
@@ -953,6 +959,8 @@ bh_status bh_advance(bh_ctx *ctx, const float *mass, const float *pos, const flo
                      float *vel_out, int where) {
   if (!ctx || !pos || nsteps < 0 || (where != BH_HOST && where != BH_DEVICE))
     return fail(ctx, BH_ERR_ARG, "bad arguments");
+  if (nsteps > 0 && peers_unordered(ctx))
+    return fail(ctx, BH_ERR_STATE, "bh_set_peers without an NCCL communicator: step with bh_step_phase");
   bh_status st = set_dev(ctx);
   if (st) return st;
   if (!ctx->io_stream) {

@@ -747,6 +747,8 @@ def test_fused_exchange_peer_stores_bitwise(BH, world, rebalance_at):
     assert np.array_equal(got_vel, ref_vel)
     with pytest.raises(Exception):
         ranks[0].step_phase(1)  # phase 1 needs a fresh phase 0
+    with pytest.raises(Exception):
+        ranks[0].step(1)  # peers without a communicator: only bh_step_phase orders the ranks
     for bh in ranks:
         bh.set_peers(None)
     o = _oracle(m, p, v, prm)
