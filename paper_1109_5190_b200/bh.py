@@ -200,8 +200,17 @@ class BarnesHut:
         if rc != BH_OK:
             raise BhError(rc, self.L.bh_last_error(self.h).decode())
 
+    def _release_peer_workspaces(self):
+        # other ranks' workspaces opened by dist.share_replicas (CUDA IPC): unmapped
+        # here, after this ctx's last store into them, never at interpreter exit
+        # (a mapping torn down after the CUDA context is gone can crash the exit)
+        if getattr(self, "_peer_workspaces", None):
+            self.sync()
+            self._peer_workspaces = None
+
     def close(self):
         if getattr(self, "h", None):
+            self._release_peer_workspaces()
             self.L.bh_destroy(self.h)
             self.h = None
 
@@ -371,6 +380,7 @@ class BarnesHut:
         address on this ctx's device (this rank's entry ignored); None = off."""
         if pos4_of_rank is None:
             self._chk(self.L.bh_set_peers(self.h, None))
+            self._release_peer_workspaces()
             return
         arr = (C.c_void_p * len(pos4_of_rank))(*[int(x) if x else None for x in pos4_of_rank])
         self._chk(self.L.bh_set_peers(self.h, C.cast(arr, C.c_void_p)))

@@ -426,7 +426,7 @@ static bh_status build_tree(bh_ctx *ctx) {
   prof_end(ctx, &pp, 8);
   prof_begin(ctx, &pp, 3);
   int launches = 0;
-  CK(launch_moments(ctx->W, n, ctx->p.theta, ctx->cont_fold, s, &launches));
+  CK(launch_moments(ctx->W, n, ctx->p.theta, (float)(ctx->p.eps * ctx->p.eps), ctx->cont_fold, s, &launches));
   prof_end(ctx, &pp, launches);
   ctx->tree_valid = true;
   return BH_OK;

@@ -36,6 +36,11 @@
 #define BH_NPHASE 6
 #define BH_MAX_PEERS 15  // bh_set_peers: replicas written by K7 besides the own one (world <= 16)
 
+// the MAC filter's thresholds in the softened domain (com.cu, walk.cu)
+#ifndef BH_EPS_FOLD
+#define BH_EPS_FOLD 1
+#endif
+
 namespace bh {
 
 #define ITEM_LEAF 0x80000000u  // item_rec flag: the item is a particle's own record
@@ -185,7 +190,7 @@ __device__ __forceinline__ void tie_run(unsigned long long kp, int64_t p, int64_
 }
 cudaError_t launch_long_runs(const Workspace &W, int64_t n, int buf, cudaStream_t s);
 cudaError_t launch_tree(const Workspace &W, int64_t n, int64_t cap_rec, int buf, int cont_fold, cudaStream_t s);
-cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont_fold, cudaStream_t s,
+cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, float eps2, int cont_fold, cudaStream_t s,
                            int *launches);
 cudaError_t launch_scan_u32(uint32_t *data, int64_t count, uint32_t *tmp, cudaStream_t s);
 cudaError_t launch_own_targets(const Workspace &W, int64_t n, int buf, uint32_t own_lo, uint32_t own_hi,

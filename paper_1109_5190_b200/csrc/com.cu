@@ -32,6 +32,20 @@
 
 #include "bh_internal.cuh"
 
+// BH_EPS_FOLD (bh_internal.cuh, default 1): the filter's thresholds are in the softened
+// domain, r2_32 = fma(dz, dz, fma(dy, dy, fma(dx, dx, eps2_32))) against
+//   T_acc = RU((A^2 + eps2_32) (1+g)),  T_rej = RD((B^2 + eps2_32) (1-g)),
+// so the walk compares the same r2 it feeds to rsqrt (one packed add fewer per
+// target pair and record).  The three fma roundings of positive terms keep the
+// relative 3u of the unsoftened sum (g unchanged), and d <= r <=> d^2 + eps^2
+// <= r^2 + eps^2, so the decisions, hence every result, are those of the exact
+// test as before.
+#ifndef BH_MOM_COMPACT
+// K5: internal nodes queued per warp (k_moments_level); 2 = where the
+// per-node work is heavy (the containment fold's radii, quadrupoles): cfg5
+// moments 3.25 -> 2.66 ms, while cfg4's light nodes lost (0.603 -> 0.645)
+#define BH_MOM_COMPACT 2
+#endif
 #ifndef BH_MOM_PREFETCH
 #define BH_MOM_PREFETCH 2  // (2 vs 1/3/4: best on cfg4 and on cfg5 with the containment fold)
 #endif
@@ -86,7 +100,7 @@ struct ContFold {
 // one internal node of level `level` at item t (record c, children [lo, hi) of the next level)
 template <bool QUAD, bool FOLD>
 __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, uint32_t lo, uint32_t hi, uint32_t off,
-                                             uint32_t off1, double r_lvl, double theta,
+                                             uint32_t off1, double r_lvl, double theta, double eps2d,
                                              const uint32_t *__restrict__ item_rec, uint32_t *__restrict__ lvl_skip,
                                              double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
                                              double *__restrict__ lvl_q,
@@ -236,9 +250,9 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     // with a safety factor 1.5 on every term
     const double b = 1.5 * u * C;
     const double A = (r * (1.0 + delta) + b) * i1ma;
-    tacc = round_up_f(A * A * (1.0 + g) * (1.0 + 4e-15));
+    tacc = round_up_f((A * A + eps2d) * (1.0 + g) * (1.0 + 4e-15));
     const double B = (r * (1.0 - delta) - b) * i1pa;
-    trej = B > 0.0 ? round_down_f(B * B * (1.0 - g) * (1.0 - 4e-15)) : -INFINITY;
+    trej = B > 0.0 ? round_down_f((B * B + eps2d) * (1.0 - g) * (1.0 - 4e-15)) : -INFINITY;
     // Levels 20-21: fp32 quantisation can place a particle up to 0.19 grid
     // quanta outside its key-space cell, so there (and only there) a cell
     // containing the target could pass s/d < theta for theta < 1/sqrt(3).
@@ -249,7 +263,7 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     if (FOLD && level < 20) {
       const double b = 1.5 * u * C;
       const double A = (Rn * (1.0 + 1e-12) + b) * i1ma;
-      tacc = Rn == INFINITY ? INFINITY : fmaxf(tacc, round_up_f(A * A * (1.0 + g) * (1.0 + 4e-15)));
+      tacc = Rn == INFINITY ? INFINITY : fmaxf(tacc, round_up_f((A * A + eps2d) * (1.0 + g) * (1.0 + 4e-15)));
     }
   }
   Rec r;
@@ -269,7 +283,7 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
                                                        const uint32_t *__restrict__ item_clo,
                                                        uint32_t *__restrict__ lvl_skip,
                                                        double4 *__restrict__ lvl_mom, Rec *__restrict__ rec,
-                                                       double theta,
+                                                       double theta, double eps2d,
                                                        double *__restrict__ lvl_q, double *__restrict__ qmom,
                                                        float4 *__restrict__ qrec, const ContFold cf) {
   if (st->err & ERR_NODE_OVERFLOW) return;
@@ -278,6 +292,52 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
   const uint32_t cnt1 = st->lvl_count[level + 1];
   const uint32_t off1 = st->lvl_offset[level + 1];
   const double r_lvl = ldexp((double)st->L, -level) / theta;  // s_l / theta
+  constexpr bool COMPACT = BH_MOM_COMPACT == 1 || (BH_MOM_COMPACT == 2 && (FOLD || QUAD));
+  if constexpr (COMPACT) {
+  // Warp compaction: most items of a level are particles (K4 finished them),
+  // so a lane per item leaves ~2/3 of the lanes idle in moments_node.  Each
+  // warp scans windows of 32 items (one coalesced load), queues the internal
+  // nodes in shared memory in item order (ballot ranks) and runs
+  // moments_node 32 queued nodes at a time with every lane busy.
+  __shared__ uint32_t s_qt[256 / 32][64], s_qe[256 / 32][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t *qt = s_qt[w], *qe = s_qe[w];
+  uint32_t qn = 0;  // warp-uniform
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  auto run = [&](uint32_t tq, uint32_t eq) {
+    const uint32_t lq = item_clo[off + tq];
+    const uint32_t hq = tq + 1 < cnt ? item_clo[off + tq + 1] : cnt1;
+    moments_node<QUAD, FOLD>(level, tq, eq, lq, hq, off, off1, r_lvl, theta, eps2d, item_rec, lvl_skip, lvl_mom, rec,
+                             lvl_q, qmom, qrec, cf, st);
+  };
+  for (uint32_t wb = (blockIdx.x * (blockDim.x >> 5) + w) * 32u; wb < cnt; wb += nwarps * 32u) {
+    const uint32_t tw = wb + lane;
+    const uint32_t ew = tw < cnt ? item_rec[off + tw] : ITEM_LEAF;
+    const bool in = !(ew & ITEM_LEAF);
+    const uint32_t bal = __ballot_sync(0xffffffffu, in);
+    if (in) {
+      const uint32_t pos = qn + __popc(bal & lt);
+      qt[pos] = tw;
+      qe[pos] = ew;
+    }
+    qn += __popc(bal);
+    __syncwarp();
+    if (qn >= 32u) {
+      const uint32_t tq = qt[lane], eq = qe[lane];
+      __syncwarp();
+      if ((uint32_t)lane < qn - 32u) {
+        qt[lane] = qt[lane + 32];
+        qe[lane] = qe[lane + 32];
+      }
+      qn -= 32u;
+      __syncwarp();
+      run(tq, eq);
+    }
+  }
+  if ((uint32_t)lane < qn) run(qt[lane], qe[lane]);
+  } else {
   // one round trip for an item, one for its children (loads hoisted so they
   // are in flight together); the next item's loads are issued before this
   // one's children are summed
@@ -302,18 +362,20 @@ __global__ void BH_MOM_BOUNDS k_moments_level(int level, const DevStatus *__rest
     lo = lon;
     hi = hin;
     if (ecur & ITEM_LEAF) continue;  // a particle: K4 wrote its record and moments
-    moments_node<QUAD, FOLD>(level, t, ecur, locur, hicur, off, off1, r_lvl, theta, item_rec, lvl_skip, lvl_mom, rec,
+    moments_node<QUAD, FOLD>(level, t, ecur, locur, hicur, off, off1, r_lvl, theta, eps2d, item_rec, lvl_skip, lvl_mom, rec,
                        lvl_q, qmom, qrec, cf, st);
+  }
   }
 }
 
 
-cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont_fold, cudaStream_t s,
+cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, float eps2, int cont_fold, cudaStream_t s,
                            int *launches) {
   ContFold cf;
   cf.lvl_rad = W.lvl_rad;
   cf.on = cont_fold;
   if (n < 2) return cudaSuccess;
+  const double eps2d = BH_EPS_FOLD ? (double)eps2 : 0.0;  // the walk's fp32 eps^2, exactly
   // grid: enough blocks for the widest level (at most n items), capped at 8
   // waves of 148 SMs
   int64_t need = (n + 255) / 256;
@@ -323,7 +385,7 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, int cont
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
 #define BH_MOM_LAUNCH(Q, F)                                                                                  \
   k_moments_level<Q, F><<<grid, 256, 0, s>>>(l, W.status, W.item_rec, W.item_clo, W.lvl_skip, W.lvl_mom, W.rec, \
-                                             theta, W.lvl_q, W.qmom, W.qrec, cf)
+                                             theta, eps2d, W.lvl_q, W.qmom, W.qrec, cf)
     if (W.qmom) {
       if (cf.on) BH_MOM_LAUNCH(true, true);
       else BH_MOM_LAUNCH(true, false);

@@ -17,6 +17,15 @@
 // lane.  The sentinel record Wn (T_acc = +inf, T_rej = -inf, skip = Wn, drop
 // word Wn + 1) parks finished groups: its targets go inactive without a drop
 // and nobody opens it, so the cursor never passes Wn and needs no clamp.
+//
+// 4 targets per lane (NP = 2, the large configurations) use the leanest form
+// (MR2): the MAC filter compares the softened r2 (BH_EPS_FOLD, com.cu), runs
+// before the rsqrt and replaces r2 by +inf for a target that does not accept
+// (rsqrt(+inf) = 0: no force, no mask multiply); the accept count stays a
+// float flag summed per pair, except for a lane's own group (GL = 1), which
+// sums rsqrt(r2m)^2 x r2 on the FMA pipe (1 +- 2^-20 or exactly 0, rounded to
+// the integer at every flush) and so spends 5 ALU-pipe instructions per
+// target and visit: ISETP, 2 FSETP, SEL (res), FSEL (r2m).
 #include "walk_common.cuh"
 
 namespace bh {
@@ -112,10 +121,71 @@ __device__ __forceinline__ void mac_accf(uint32_t cc, float d2, float tacc, floa
       : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
 }
 
+// BH_MASK_R2: the same, and r2 replaced by +inf for a target that does not
+// accept (rsqrt(+inf) = 0: the force vanishes without the mask multiply)
+__device__ __forceinline__ void mac_accf_r2(uint32_t cc, float d2, float tacc, float trej, uint32_t skip,
+                                            uint32_t dropw, uint32_t &res, float &accf, float &r2m) {
+  asm("{\n\t.reg .pred pa, pc, pq;\n\t"
+      "setp.ge.u32 pa, %3, %0;\n\t"
+      "setp.gt.and.f32 pc, %4, %5, pa;\n\t"
+      "setp.ge.and.f32 pq, %4, %6, pa;\n\t"
+      "@pq selp.b32 %0, %7, %8, pc;\n\t"
+      "selp.f32 %1, 0f3F800000, 0f00000000, pc;\n\t"
+      "selp.f32 %2, %4, 0f7F800000, pc;\n\t}"
+      : "+r"(res), "=f"(accf), "=f"(r2m)
+      : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
+}
+// (2 = for 4 targets per lane only: cfg4 walk 39.5 -> 38.2 ms, cfg5 66.0 -> 65.3,
+// cfg3 0.705 -> 0.690; 2 targets per lane lost, cfg2 0.605 -> 0.623)
+// ... and the count as an integer (a predicated add in place of the float
+// flag: no FADD2 per pair, the same ALU count)
+__device__ __forceinline__ void mac_cnt_r2(uint32_t cc, float d2, float tacc, float trej, uint32_t skip,
+                                           uint32_t dropw, uint32_t &res, uint32_t &cnt, float &r2m) {
+  asm("{\n\t.reg .pred pa, pc, pq;\n\t"
+      "setp.ge.u32 pa, %3, %0;\n\t"
+      "setp.gt.and.f32 pc, %4, %5, pa;\n\t"
+      "setp.ge.and.f32 pq, %4, %6, pa;\n\t"
+      "@pq selp.b32 %0, %7, %8, pc;\n\t"
+      "@pc add.u32 %1, %1, 1;\n\t"
+      "selp.f32 %2, %4, 0f7F800000, pc;\n\t}"
+      : "+r"(res), "+r"(cnt), "=f"(r2m)
+      : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
+}
+// ... and no flag at all: the count is summed as rsqrt(r2m)^2 x r2 on the FMA
+// pipe (BH_MR2_FCNT: 1 +- 2^-20 for an accept, exactly 0 otherwise; rounded
+// to the integer at every flush, <= 48 terms per block)
+__device__ __forceinline__ void mac_r2(uint32_t cc, float d2, float tacc, float trej, uint32_t skip,
+                                       uint32_t dropw, uint32_t &res, float &r2m) {
+  asm("{\n\t.reg .pred pa, pc, pq;\n\t"
+      "setp.ge.u32 pa, %2, %0;\n\t"
+      "setp.gt.and.f32 pc, %3, %4, pa;\n\t"
+      "setp.ge.and.f32 pq, %3, %5, pa;\n\t"
+      "@pq selp.b32 %0, %6, %7, pc;\n\t"
+      "selp.f32 %1, %3, 0f7F800000, pc;\n\t}"
+      : "+r"(res), "=f"(r2m)
+      : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
+}
+// (2 = a lane's own group only: cfg5 walk 65.31 -> 65.03 ms; with 2-lane
+// groups it lost, cfg4 38.19 -> 38.64, though it issues 63 instead of 66
+// instructions per visit: the FMA pipe, not issue, binds there)
+#ifndef BH_MR2_FCNT
+#define BH_MR2_FCNT 2
+#endif
+#ifndef BH_MR2_INTCNT
+#define BH_MR2_INTCNT 0  // (1: ptxas materialises the predicates, 74 vs 66 instructions per visit)
+#endif
+#ifndef BH_MASK_R2
+#define BH_MASK_R2 2
+#endif
+
 // STATS: also count the opened MAC tests (the flop model of bench.py).
 template <int GL, int NP, bool CONT, bool QUAD, bool STATS>
 __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_MINB : BH_WALK_MINB2)) k_walk(const WalkParams P) {
   constexpr int TPL = 2 * NP;              // targets per lane (NP packed pairs)
+  // the force mask on r2 (BH_MASK_R2, 4 targets per lane by default)
+  constexpr bool MR2 = (BH_MASK_R2 == 1 || (BH_MASK_R2 == 2 && NP == 2)) && BH_EPS_FOLD && !CONT && !QUAD;
+  constexpr bool MFC = MR2 && (BH_MR2_FCNT == 1 || (BH_MR2_FCNT == 2 && GL == 1));  // count = rsqrt^2 x r2
+  constexpr bool FCNT = !CONT && !(MR2 && !MFC && BH_MR2_INTCNT);  // float accept counts (flushed every BH_FOLD_TRIPS)
   constexpr int GT = GL * TPL;             // targets per group
   constexpr int GPB = BH_WALK_BLOCK / GL;  // groups per block
   const uint32_t full = 0xffffffffu;
@@ -235,14 +305,50 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
       for (int j = 0; j < NP; j++) {
         const int ka = 2 * j, kb = 2 * j + 1;
         const F2 DX = sub2(pk2(cm.x, cm.x), X[j]), DY = sub2(pk2(cm.y, cm.y), Y[j]), DZ = sub2(pk2(cm.z, cm.z), Z[j]);
+#if BH_EPS_FOLD
+        // the softened distance, which the MAC filter compares too (com.cu)
+        const F2 R2 = fma2(DZ, DZ, fma2(DY, DY, fma2(DX, DX, E2)));
+        float r2A, r2B;
+        up2(R2, r2A, r2B);
+        const float d2A = r2A, d2B = r2B;
+#else
         const F2 D2 = fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX)));
         float d2A, d2B;
         up2(D2, d2A, d2B);
-        // the interaction of both targets, branch-free (f zeroed for a target
-        // that does not accept the record)
         float r2A, r2B;
         const F2 R2 = add2(D2, E2);
         up2(R2, r2A, r2B);
+#endif
+        if constexpr (MR2) {
+          // the MAC first; a target that does not accept gets r2 = +inf, so
+          // its rsqrt and force are 0 (no mask multiply)
+          float rmA, rmB;
+          if constexpr (MFC) {
+            mac_r2(cc, r2A, tacc, trej, skip, dropw, res[ka], rmA);
+            mac_r2(cc, r2B, tacc, trej, skip, dropw, res[kb], rmB);
+          } else if constexpr (BH_MR2_INTCNT) {
+            mac_cnt_r2(cc, r2A, tacc, trej, skip, dropw, res[ka], cnt[ka], rmA);
+            mac_cnt_r2(cc, r2B, tacc, trej, skip, dropw, res[kb], cnt[kb], rmB);
+          } else {
+            float accA, accB;
+            mac_accf_r2(cc, r2A, tacc, trej, skip, dropw, res[ka], accA, rmA);
+            mac_accf_r2(cc, r2B, tacc, trej, skip, dropw, res[kb], accB, rmB);
+            CNT[j] = add2(CNT[j], pk2(accA, accB));
+          }
+          const F2 INV = pk2(rsqrt_fast(rmA), rsqrt_fast(rmB));
+          const F2 INV2 = mul2(INV, INV);
+          if constexpr (MFC) CNT[j] = fma2(INV2, R2, CNT[j]);
+          const F2 FF = mul2(mul2(pk2(cm.w, cm.w), INV2), INV);
+          asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+              : "+f"(ax[ka]), "+f"(ax[kb]) : "l"(FF.v), "l"(DX.v));
+          asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+              : "+f"(ay[ka]), "+f"(ay[kb]) : "l"(FF.v), "l"(DY.v));
+          asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%0, %1};\n\tfma.rn.f32x2 t, %2, %3, t;\n\tmov.b64 {%0, %1}, t;\n\t}"
+              : "+f"(az[ka]), "+f"(az[kb]) : "l"(FF.v), "l"(DZ.v));
+          continue;
+        }
+        // the interaction of both targets, branch-free (f zeroed for a target
+        // that does not accept the record)
 #if BH_RSQRT_NEWTON
         // (accuracy experiment: one Newton step on MUFU.RSQ, y (1.5 - 0.5 r2 y^2))
         F2 INV = pk2(rsqrt_fast(r2A), rsqrt_fast(r2B));
@@ -342,17 +448,17 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
     git += live ? 1u : 0u;
     if (++trip == BH_FOLD_TRIPS) {  // warp-uniform
       trip = 0;
-      if (!CONT) {  // the fp32 counts (<= 3 x BH_FOLD_TRIPS each) into the integer ones
+      if (FCNT) {  // the fp32 counts (<= 3 x BH_FOLD_TRIPS each) into the integer ones
 #pragma unroll
         for (int j = 0; j < NP; j++) {
           float ca, cb;
           up2(CNT[j], ca, cb);
           if constexpr (FM == 3) {
-            s_cnt[2 * j][threadIdx.x] += (uint32_t)ca;
-            s_cnt[2 * j + 1][threadIdx.x] += (uint32_t)cb;
+            s_cnt[2 * j][threadIdx.x] += __float2uint_rn(ca);
+            s_cnt[2 * j + 1][threadIdx.x] += __float2uint_rn(cb);
           } else {
-            cnt[2 * j] += (uint32_t)ca;
-            cnt[2 * j + 1] += (uint32_t)cb;
+            cnt[2 * j] += __float2uint_rn(ca);
+            cnt[2 * j + 1] += __float2uint_rn(cb);
           }
           CNT[j] = pk2(0.f, 0.f);
         }
@@ -386,13 +492,13 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
     else { T[k].p = 0; T[k].Li = 0; T[k].s = 0; T[k].me = make_float4(0.f, 0.f, 0.f, 0.f); }
     own[k] = v[k] && (!P.own_check || (T[k].s >= P.own_lo && T[k].s < P.own_hi));
   }
-  if (!CONT) {
+  if (FCNT) {
 #pragma unroll
     for (int j = 0; j < NP; j++) {
       float ca, cb;
       up2(CNT[j], ca, cb);
-      cnt[2 * j] += (uint32_t)ca;
-      cnt[2 * j + 1] += (uint32_t)cb;
+      cnt[2 * j] += __float2uint_rn(ca);
+      cnt[2 * j + 1] += __float2uint_rn(cb);
       if constexpr (FM == 3) {
         cnt[2 * j] += s_cnt[2 * j][threadIdx.x];
         cnt[2 * j + 1] += s_cnt[2 * j + 1][threadIdx.x];

@@ -44,7 +44,13 @@ __device__ __forceinline__ bool resume_visit(const WalkParams &P, const Target &
   const uint4 au = P.rec[c].aux;
   skip = au.z;
   const float dx = __fsub_rn(cm.x, T.me.x), dy = __fsub_rn(cm.y, T.me.y), dz = __fsub_rn(cm.z, T.me.z);
+#if BH_EPS_FOLD
+  const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmaf_rn(dx, dx, P.eps2)));  // softened (com.cu)
+  const float r2 = d2;
+#else
   const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+  const float r2 = __fadd_rn(d2, P.eps2);
+#endif
   const bool cont = (c <= T.Li) & (au.z > T.Li);
   bool acc = !cont & (d2 > __uint_as_float(au.x));
   if (!cont && !acc && d2 >= __uint_as_float(au.y)) {
@@ -52,7 +58,7 @@ __device__ __forceinline__ bool resume_visit(const WalkParams &P, const Target &
     A.fb++;
   }
   if (acc) {
-    const float inv = rsqrt_fast(__fadd_rn(d2, P.eps2));
+    const float inv = rsqrt_fast(r2);
     const float f = __fmul_rn(__fmul_rn(cm.w, __fmul_rn(inv, inv)), inv);
     A.ax += (double)__fmul_rn(f, dx);
     A.ay += (double)__fmul_rn(f, dy);
