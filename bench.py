@@ -258,7 +258,7 @@ def ours_arm(args):
     bh.step(args.warmup)
     bh.sync()
     if world > 1 and not args.no_rebalance:
-        # equal-cost ownership from the warm-up's interaction counts (dist.rebalance),
+        # equal-cost ownership from the warm-up's walk trips (dist.rebalance),
         # then one more untimed step on the new partition
         try:
             bounds = bdist.rebalance(bh, dist, device=f"cuda:{device}")
@@ -290,7 +290,7 @@ def ours_arm(args):
         ev0.record(stream)
         for k in range(args.steps):
             if world > 1 and args.rebalance_every > 0 and k > 0 and k % args.rebalance_every == 0:
-                # NEXT-2: equal-cost ownership from the last walk's counts, inside the
+                # NEXT-2: equal-cost ownership from the last walk's trips, inside the
                 # timed region (host collectives: its cost is part of the step)
                 bdist.rebalance(bh, dist, device=f"cuda:{device}")
             bh.step(1)

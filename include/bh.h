@@ -192,6 +192,14 @@ bh_status bh_get_interactions(bh_ctx *ctx, uint32_t *count, uint64_t *total);
  *   replicated and unaffected; results do not depend on the partition.  Syncs. */
 bh_status bh_get_own(bh_ctx *ctx, uint32_t *icount, float *vel, int where);
 
+/* bh_get_own_cost: trips[own] = the loop trips of the walk group each own
+ * particle was last walked in (storage order, uint32[own_hi - own_lo]; 0
+ * before the first walk) -- a walk-TIME cost estimate: a rank's walk time
+ * follows the summed trips of its groups more closely than their interaction
+ * counts.  Ownership-balancing input for bh_set_partition.
+ * where = BH_HOST / BH_DEVICE.  Syncs. */
+bh_status bh_get_own_cost(bh_ctx *ctx, uint32_t *trips, int where);
+
 /* multipole = 2: the fp64 quadrupoles of the tree nodes in bh_get_tree's order,
  * Q[node][6] = (xx, yy, zz, xy, xz, yz) about the node's centre of mass
  * (particles: 0).  Q may be NULL to query *n_nodes.  Syncs. */

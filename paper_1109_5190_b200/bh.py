@@ -104,6 +104,7 @@ def load_library(path: str = LIB_PATH):
             "bh_get_moments": (i32, [vp, vp, vp, i64]),
             "bh_get_interactions": (i32, [vp, vp, vp]),
             "bh_get_own": (i32, [vp, vp, vp, i32]),
+            "bh_get_own_cost": (i32, [vp, vp, i32]),
             "bh_get_quadrupoles": (i32, [vp, vp, i64, C.POINTER(i64)]),
             "bh_get_pos4": (i32, [vp, vp, i64, i64, i32]),
             "bh_set_pos4": (i32, [vp, vp, i64, i64, i32]),
@@ -358,6 +359,15 @@ class BarnesHut:
         v = np.zeros((m, 3), np.float32)
         self._chk(self.L.bh_get_own(self.h, _ptr(c), _ptr(v), BH_HOST))
         return c, v
+
+    def get_own_cost(self):
+        """trips[own]: the last walk's loop trips of each own particle's group
+        (bh_get_own_cost; the walk-time cost for dist.rebalance)."""
+        st = self.get_stats()
+        m = int(st["own_end"] - st["own_begin"])
+        t = np.zeros(m, np.uint32)
+        self._chk(self.L.bh_get_own_cost(self.h, _ptr(t), BH_HOST))
+        return t
 
     def get_pos4(self, lo, hi):
         """Storage-order slice [lo, hi) of the replicated (x, y, z, m)."""

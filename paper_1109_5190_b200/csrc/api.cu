@@ -1204,6 +1204,17 @@ bh_status bh_get_own(bh_ctx *ctx, uint32_t *icount, float *vel, int where) {
   return do_sync(ctx);
 }
 
+bh_status bh_get_own_cost(bh_ctx *ctx, uint32_t *trips, int where) {
+  if (!ctx || !trips || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
+  bh_status st = set_dev(ctx);
+  if (st) return st;
+  const int64_t lo = ctx->own_lo, own_n = ctx->own_hi - ctx->own_lo;
+  if (own_n)
+    CK(cudaMemcpyAsync(trips, ctx->W.gcost + lo, (size_t)own_n * 4,
+                       where == BH_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+  return do_sync(ctx);
+}
+
 bh_status bh_set_partition(bh_ctx *ctx, const int64_t *bounds, const float *vel, int where) {
   if (!ctx || !bounds || (where != BH_HOST && where != BH_DEVICE)) return fail(ctx, BH_ERR_ARG, "bad arguments");
   const int P = ctx->p.world, r = ctx->p.rank;

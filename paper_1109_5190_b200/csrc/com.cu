@@ -46,6 +46,9 @@
 // moments 3.25 -> 2.66 ms, while cfg4's light nodes lost (0.603 -> 0.645)
 #define BH_MOM_COMPACT 2
 #endif
+#ifndef BH_TIGHT_COM
+#define BH_TIGHT_COM 1
+#endif
 #ifndef BH_MOM_PREFETCH
 #define BH_MOM_PREFETCH 2  // (2 vs 1/3/4: best on cfg4 and on cfg5 with the containment fold)
 #endif
@@ -247,8 +250,18 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     C = sqrt((double)fx * fx + (double)fy * fy + (double)fz * fz);
     // first-order bounds (u: com rounding |c32 - c64| <= u(1+u)|c32|, one
     // rounding of the subtraction, <= 3 roundings in the fp32 sum of squares)
-    // with a safety factor 1.5 on every term
+    // with a safety factor 1.5 on every term.  BH_TIGHT_COM: the com term is
+    // the node's actual rounding displacement |c32 - c64| instead of its
+    // bound (c32 - c64 is exact in fp64; its norm is padded by 1e-6 relative,
+    // and 1e-15 |c| covers c64's reciprocal against the oracle's quotient,
+    // <= 2.5 fp64 ulp per axis) -- on average ~3x narrower, and it dominates
+    // the band wherever r << |c| (cfg5: 100x the subtraction term at level 10)
+#if BH_TIGHT_COM
+    const double ex = (double)fx - cx, ey = (double)fy - cy, ez = (double)fz - cz;
+    const double b = sqrt(ex * ex + ey * ey + ez * ez) * (1.0 + 1e-6) + 1e-15 * C;
+#else
     const double b = 1.5 * u * C;
+#endif
     const double A = (r * (1.0 + delta) + b) * i1ma;
     tacc = round_up_f((A * A + eps2d) * (1.0 + g) * (1.0 + 4e-15));
     const double B = (r * (1.0 - delta) - b) * i1pa;
@@ -261,7 +274,6 @@ __device__ __forceinline__ void moments_node(int level, uint32_t t, uint32_t c, 
     // re-walk, which tests containment.
     if (level >= 20) tacc = INFINITY;
     if (FOLD && level < 20) {
-      const double b = 1.5 * u * C;
       const double A = (Rn * (1.0 + 1e-12) + b) * i1ma;
       tacc = Rn == INFINITY ? INFINITY : fmaxf(tacc, round_up_f((A * A + eps2d) * (1.0 + g) * (1.0 + 4e-15)));
     }

@@ -62,10 +62,12 @@ def cost_bounds(costs, world: int):
     return b
 
 
-def rebalance(bh, dist, device=None):
-    """Collective: gather every rank's per-particle costs (the last walk's
-    interaction counts) and velocities, compute equal-cost bounds, and hand each
-    rank its new range and velocities (bh_set_partition).  Returns the bounds."""
+def rebalance(bh, dist, device=None, cost="trips"):
+    """Collective: gather every rank's per-particle costs and velocities,
+    compute equal-cost bounds, and hand each rank its new range and velocities
+    (bh_set_partition).  Returns the bounds.  cost = "trips": the last walk's
+    loop trips of each particle's group (bh_get_own_cost: walk time), or
+    "interactions": its interaction count (bh_get_own)."""
     import numpy as np
     import torch
 
@@ -73,6 +75,8 @@ def rebalance(bh, dist, device=None):
     st = bh.get_stats()
     lo, hi = int(st["own_begin"]), int(st["own_end"])
     cnt, vel = bh.get_own()
+    if cost == "trips":
+        cnt = bh.get_own_cost()
     sizes = [None] * world
     dist.all_gather_object(sizes, (lo, hi))
     m = max(h - l for l, h in sizes)

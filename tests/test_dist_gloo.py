@@ -116,6 +116,9 @@ class _FakeBH:
     def get_own(self):
         return self.costs[self.lo:self.hi].astype(np.uint32), self.vel[self.lo:self.hi]
 
+    def get_own_cost(self):  # the walk-trip costs (dist.rebalance's default)
+        return self.costs[self.lo:self.hi].astype(np.uint32)
+
     def set_partition(self, bounds, vel_own):
         self.got = (list(bounds), np.array(vel_own))
 

@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--fused", action="store_true")
     ap.add_argument("--rebalance", action="store_true", help="--fused: equal-cost ownership after the warm-up")
+    ap.add_argument("--cost", default="trips", choices=["trips", "interactions"],
+                    help="--rebalance: per-particle cost (dist.rebalance's; trips = the group's walk loop trips)")
     a = ap.parse_args()
     from paper_1109_5190_b200 import BarnesHut
 
@@ -107,12 +109,13 @@ def fused_row(BarnesHut, m, p, v, prm, P, a, cfg, t1):
         from paper_1109_5190_b200 import dist as bdist
 
         own = [bh.get_own() for bh in ranks]
-        bounds = bdist.cost_bounds(np.concatenate([c for c, _ in own]).astype(np.float64), P)
+        costs = [bh.get_own_cost() for bh in ranks] if a.cost == "trips" else [c for c, _ in own]
+        bounds = bdist.cost_bounds(np.concatenate(costs).astype(np.float64), P)
         vels = np.concatenate([v_ for _, v_ in own])
         for r, bh in enumerate(ranks):
             bh.set_partition(bounds, vels[bounds[r]:bounds[r + 1]])
         one_step()
-        balance = "cost split after the warm-up"
+        balance = f"cost split after the warm-up ({a.cost})"
     for bh in ranks:
         bh.set_profiling(True)
     for _ in range(a.steps):
