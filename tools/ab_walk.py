@@ -34,7 +34,7 @@ def main():
     cfg = sys.argv[1]
     m, p, v = bhgen.generate(cfg)
     np.savez("/tmp/ab_in.npz", m=m, p=p, v=v)
-    prm = bhgen.params(cfg)
+    prm = dict(bhgen.params(cfg), **json.loads(os.environ.get("AB_PRM", "{}")))  # e.g. AB_PRM='{"walk_group": 70}'
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for rep in range(2):
         for lib in sys.argv[2:]:
