@@ -7,6 +7,7 @@
 //   fix-up) -> K4 LCP / record counts / scan / emit -> K5 22 level passes ->
 //   [world > 1: owned-target compaction] -> K6+K7 walk + leapfrog ->
 //   [world > 1: K8 grouped ncclBroadcast of every rank's slice of pos4].
+#include <float.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdarg.h>
@@ -304,6 +305,9 @@ __global__ void k_scatter1(uint32_t *__restrict__ out, const uint32_t *__restric
 }  // namespace bh
 
 // ---------------------------------------------------------------- helpers
+// eps > 0 as the walk sees it: fp32 eps^2 a normal number (eps >~ 1.1e-19)
+static bool eps2_normal(double eps) { return (float)(eps * eps) >= FLT_MIN; }
+
 static unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1); }
 
 static bh_status validate(const bh_params *p, char *err, size_t errn) {
@@ -460,8 +464,10 @@ static bh_status walk(bh_ctx *ctx, int mode, float kick, float *acc_out, bool us
   a.num_sms = ctx->num_sms;
   // containment test elision (see walk.cu): a cell holding the target has
   // s/d >= 1/sqrt(3) (d <= sqrt(3) s), so it never passes s/d < theta for
-  // theta < 0.5773; kept with a margin, and only when eps > 0
-  a.need_cont = !(ctx->p.theta < 0.57 && ctx->p.eps > 0.0) && !ctx->cont_fold;
+  // theta < 0.5773; kept with a margin, and only when eps > 0 -- as the walk's
+  // fp32 eps^2, a normal float, so every unmasked force is finite (rsqrt of a
+  // zero or flushed-denormal r2 would be inf, and 0 x inf a NaN)
+  a.need_cont = !(ctx->p.theta < 0.57 && eps2_normal(ctx->p.eps)) && !ctx->cont_fold;
   a.mode = mode;
   a.eps2 = (float)(ctx->p.eps * ctx->p.eps);
   a.G = (float)ctx->p.G;
@@ -617,7 +623,7 @@ bh_status bh_create(bh_ctx **out, const bh_params *p, const float *mass, const f
   ctx->use_graphs = getenv("BH_NO_GRAPHS") ? 0 : 1;
   // the near-sorted path pays for its ~20 launches from ~2^18 particles on
   // (measured: cfg2, 2^16, 2% slower with it; cfg3, 2^20, 7% faster)
-  ctx->cont_fold = (p->theta >= 0.57 && p->eps > 0.0 && !getenv("BH_NO_CONT_FOLD")) ? 1 : 0;
+  ctx->cont_fold = (p->theta >= 0.57 && eps2_normal(p->eps) && !getenv("BH_NO_CONT_FOLD")) ? 1 : 0;
   ctx->near_sort = getenv("BH_NO_NEAR_SORT") ? 0 : (p->n >= ((int64_t)1 << 18) || getenv("BH_NEAR_SORT") ? 1 : 0);
   ctx->step_graph[0] = ctx->step_graph[1] = ctx->step_graph[2] = nullptr;
   ctx->num_sms = 148;

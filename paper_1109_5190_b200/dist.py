@@ -62,12 +62,30 @@ def cost_bounds(costs, world: int):
     return b
 
 
-def rebalance(bh, dist, device=None, cost="trips"):
+def time_scaled(costs, walk_ms):
+    """One rank's per-particle costs rescaled so that they sum to the rank's
+    measured walk time (ms per step): the equal-cost split of the rescaled
+    costs then balances measured time, not a proxy -- time per walk trip
+    differs between Morton ranges.  Unchanged without a time
+    or with zero costs."""
+    import numpy as np
+
+    c = np.asarray(costs, dtype=np.float64)
+    tot = float(c.sum())
+    if walk_ms is None or not (walk_ms > 0.0) or not (tot > 0.0):
+        return c
+    return c * (float(walk_ms) / tot)
+
+
+def rebalance(bh, dist, device=None, cost="trips", walk_ms=None):
     """Collective: gather every rank's per-particle costs and velocities,
     compute equal-cost bounds, and hand each rank its new range and velocities
     (bh_set_partition).  Returns the bounds.  cost = "trips": the last walk's
     loop trips of each particle's group (bh_get_own_cost: walk time), or
-    "interactions": its interaction count (bh_get_own)."""
+    "interactions": its interaction count (bh_get_own).  walk_ms (this rank's
+    measured walk time per step, e.g. from bh_get_profile): the costs are
+    rescaled to it first (time_scaled), so repeated calls converge on equal
+    measured walk times."""
     import numpy as np
     import torch
 
@@ -77,12 +95,13 @@ def rebalance(bh, dist, device=None, cost="trips"):
     cnt, vel = bh.get_own()
     if cost == "trips":
         cnt = bh.get_own_cost()
+    cnt = time_scaled(cnt, walk_ms)
     sizes = [None] * world
     dist.all_gather_object(sizes, (lo, hi))
     m = max(h - l for l, h in sizes)
     pad_c = torch.zeros(m, dtype=torch.float64, device=device)
     pad_v = torch.zeros((m, 3), dtype=torch.float32, device=device)
-    pad_c[: hi - lo] = torch.from_numpy(cnt.astype(np.float64)).to(device)
+    pad_c[: hi - lo] = torch.from_numpy(np.asarray(cnt, dtype=np.float64)).to(device)
     pad_v[: hi - lo] = torch.from_numpy(vel).to(device)
     all_c = [torch.empty_like(pad_c) for _ in range(world)]
     all_v = [torch.empty_like(pad_v) for _ in range(world)]

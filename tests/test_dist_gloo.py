@@ -123,6 +123,27 @@ class _FakeBH:
         self.got = (list(bounds), np.array(vel_own))
 
 
+def test_time_scaled_costs():
+    """dist.time_scaled: a rank's costs rescaled to its measured walk time.
+    Two ranks with equal summed costs but rank 1 twice as slow per unit:
+    after rescaling, the equal-cost split moves work from rank 1 to rank 0
+    so that the predicted times (cost x the rank's time per unit) equalise."""
+    c = np.full(1000, 3.0)
+    t = bdist.time_scaled(c, 6.0)
+    assert np.isclose(t.sum(), 6.0) and np.allclose(t, t[0])
+    assert np.array_equal(bdist.time_scaled(c, None), c)
+    assert np.array_equal(bdist.time_scaled(np.zeros(5), 2.0), np.zeros(5))
+    # per-unit speeds 1 (rank 0's half) and 2 (rank 1's half), equal costs
+    n = 2000
+    costs = np.ones(n)
+    walk = [1000.0, 2000.0]  # measured ms of the halves
+    scaled = np.concatenate([bdist.time_scaled(costs[:1000], walk[0]), bdist.time_scaled(costs[1000:], walk[1])])
+    b = bdist.cost_bounds(scaled, 2)
+    t0 = scaled[: b[1]].sum()
+    t1 = scaled[b[1]:].sum()
+    assert b[1] > 1000 and abs(t0 - t1) <= scaled.max() + 1e-9
+
+
 def _rebalance_worker(rank, world, port, n, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

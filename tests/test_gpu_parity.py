@@ -189,6 +189,26 @@ def test_ragged_and_tiny_sizes(BH, n):
     assert relerr(bh.get_state()[0], o.state()[0]).max() < TOL
 
 
+@pytest.mark.parametrize("theta", [0.5, 0.7])
+def test_eps_below_fp32_square(BH, theta):
+    """eps > 0 whose fp32 square is zero (eps = 1e-25): the walk's fast paths
+    that rely on a finite unmasked force (no per-visit containment test, the
+    force mask on r2) must not run, since rsqrt(0) is inf and 0 x inf a NaN
+    (api.cu eps2_normal); forces and 2 steps still match the oracle."""
+    n = 6000
+    m, p, v = bhgen.generate("cfg3", n=n)
+    prm = dict(theta=theta, eps=1e-25, G=1.0, dt=1e-6)
+    bh = BH(m, p, v, walk_group=69, **prm)
+    bh.build_tree()
+    o = _oracle(m, p, v, prm)
+    check_step0(bh, o, n)
+    bh.step(2)
+    o.step(2)
+    pos = bh.get_state()[0]
+    assert np.isfinite(pos).all()
+    assert relerr(pos, o.state()[0]).max() < TOL
+
+
 def test_buckets_duplicates_coincident(BH):
     rng = np.random.default_rng(1)
     base = rng.random((3000, 3)).astype(np.float32)

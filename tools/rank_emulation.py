@@ -47,8 +47,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--fused", action="store_true")
     ap.add_argument("--rebalance", action="store_true", help="--fused: equal-cost ownership after the warm-up")
-    ap.add_argument("--cost", default="trips", choices=["trips", "interactions"],
-                    help="--rebalance: per-particle cost (dist.rebalance's; trips = the group's walk loop trips)")
+    ap.add_argument("--cost", default="trips", choices=["trips", "interactions", "time"],
+                    help="--rebalance: per-particle cost (dist.rebalance's; trips = the group's walk loop trips; "
+                         "time = trips rescaled per rank to its measured walk time, --rounds times)")
+    ap.add_argument("--rounds", type=int, default=2, help="--cost time: feedback rounds")
     a = ap.parse_args()
     from paper_1109_5190_b200 import BarnesHut
 
@@ -108,13 +110,23 @@ def fused_row(BarnesHut, m, p, v, prm, P, a, cfg, t1):
 
         from paper_1109_5190_b200 import dist as bdist
 
-        own = [bh.get_own() for bh in ranks]
-        costs = [bh.get_own_cost() for bh in ranks] if a.cost == "trips" else [c for c, _ in own]
-        bounds = bdist.cost_bounds(np.concatenate(costs).astype(np.float64), P)
-        vels = np.concatenate([v_ for _, v_ in own])
-        for r, bh in enumerate(ranks):
-            bh.set_partition(bounds, vels[bounds[r]:bounds[r + 1]])
-        one_step()
+        for rnd in range(a.rounds if a.cost == "time" else 1):
+            walk = [None] * P
+            if a.cost == "time":  # one profiled step: each rank's measured walk time
+                for bh in ranks:
+                    bh.set_profiling(True)
+                one_step()
+                for r, bh in enumerate(ranks):
+                    walk[r] = bh.get_profile()["ms"]["walk"]
+                    bh.set_profiling(False)
+            own = [bh.get_own() for bh in ranks]
+            costs = [bh.get_own_cost() for bh in ranks] if a.cost != "interactions" else [c for c, _ in own]
+            costs = [bdist.time_scaled(c, walk[r]) for r, c in enumerate(costs)]
+            bounds = bdist.cost_bounds(np.concatenate(costs).astype(np.float64), P)
+            vels = np.concatenate([v_ for _, v_ in own])
+            for r, bh in enumerate(ranks):
+                bh.set_partition(bounds, vels[bounds[r]:bounds[r + 1]])
+            one_step()
         balance = f"cost split after the warm-up ({a.cost})"
     for bh in ranks:
         bh.set_profiling(True)
