@@ -258,10 +258,17 @@ def ours_arm(args):
     bh.step(args.warmup)
     bh.sync()
     if world > 1 and not args.no_rebalance:
-        # equal-cost ownership from the warm-up's walk trips (dist.rebalance),
-        # then one more untimed step on the new partition
+        # equal-cost ownership: the walk trips of each particle's group, rescaled
+        # per rank to its measured walk time (dist.time_scaled; two feedback
+        # rounds, each from one profiled untimed step), then one more untimed
+        # step on the new partition
         try:
-            bounds = bdist.rebalance(bh, dist, device=f"cuda:{device}")
+            for _ in range(2):
+                bh.set_profiling(True)
+                bh.step(1)
+                walk_ms = bh.get_profile()["ms"]["walk"]
+                bh.set_profiling(False)
+                bounds = bdist.rebalance(bh, dist, device=f"cuda:{device}", walk_ms=walk_ms)
             if rank == 0:
                 print(f"rebalanced ownership: {bounds}", file=sys.stderr)
         except Exception as e:  # keep the even split
