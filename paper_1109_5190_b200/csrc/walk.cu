@@ -40,7 +40,7 @@ namespace bh {
 #define BH_WALK_UNROLL 2  // record visits per loop trip, groups of >= 4 lanes
 #endif
 #ifndef BH_WALK_UNROLL_NP2
-#define BH_WALK_UNROLL_NP2 3  // 4 targets per lane
+#define BH_WALK_UNROLL_NP2 4  // 4 targets per lane (4 vs 3, with 32-trip blocks: cfg4 walk 38.05 -> 37.75 ms, cfg5 63.99 -> 63.13)
 #endif
 #ifndef BH_WALK_UNROLL_SMALL
 #define BH_WALK_UNROLL_SMALL 3  // groups of <= 2 lanes (3 vs 2: cfg5 -2.2%, cfg3 -1.2%, cfg2 -1.4%, r1)
@@ -66,7 +66,7 @@ namespace bh {
 #define BH_RSQRT_NEWTON 0
 #endif
 #ifndef BH_FOLD_TRIPS
-#define BH_FOLD_TRIPS 16
+#define BH_FOLD_TRIPS 32  // (16 before r2z; 32 measured: cfg4 max error 1.6e-5, cfg5 6.7e-5 -- its per-term floor)
 #endif
 #ifndef BH_WALK_MINB2
 #define BH_WALK_MINB2 7  // NP = 2 (4 targets per lane): 72 registers, no spill in the loop (8 blocks: 64, cfg4 +4.5%)
@@ -153,7 +153,7 @@ __device__ __forceinline__ void mac_cnt_r2(uint32_t cc, float d2, float tacc, fl
 }
 // ... and no flag at all: the count is summed as rsqrt(r2m)^2 x r2 on the FMA
 // pipe (BH_MR2_FCNT: 1 +- 2^-20 for an accept, exactly 0 otherwise; rounded
-// to the integer at every flush, <= 48 terms per block)
+// to the integer at every flush, <= 128 terms per block: error < 2e-3)
 __device__ __forceinline__ void mac_r2(uint32_t cc, float d2, float tacc, float trej, uint32_t skip,
                                        uint32_t dropw, uint32_t &res, float &r2m) {
   asm("{\n\t.reg .pred pa, pc, pq;\n\t"
