@@ -97,6 +97,10 @@ __device__ __forceinline__ uint32_t match8(uint32_t act, uint32_t dig) {
 // (st->near_ok); SORT_BAD sorts the near-sorted path's st->n_bad out-of-order
 // keys and runs only if that path is still on.
 enum { SORT_FULL = 0, SORT_BAD = 1 };
+#ifndef BH_SORT_PERSIST
+#define BH_SORT_PERSIST 1
+#endif
+constexpr int64_t SORT_PERSIST_GRID = 2 * 148;  // 2 CTAs per SM (__launch_bounds__ below)
 
 __global__ void __launch_bounds__(SORT_BLOCK, 2) k_onesweep(const unsigned long long *__restrict__ kin,
                                                          const uint32_t *__restrict__ vin,
@@ -115,12 +119,19 @@ __global__ void __launch_bounds__(SORT_BLOCK, 2) k_onesweep(const unsigned long 
   const int64_t need = n > 0 ? (n + SORT_TILE - 1) / SORT_TILE : 1;
   if ((int64_t)blockIdx.x >= need) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // BH_SORT_PERSIST: a grid of at most 2 CTAs per SM, each taking tickets
+  // until they run out (tiles in ticket order, so the look-back only waits on
+  // tiles that running CTAs hold); a pass that does not run -- the full path
+  // of a near-sorted build, the bad-key path's capacity tail -- costs ~300
+  // CTAs that leave at once instead of one per tile
+  for (;;) {
   if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
   for (int i = tid; i < SORT_WARPS * SORT_RADIX; i += SORT_BLOCK) (&S.wcount[0][0])[i] = 0;
   __syncthreads();
   const uint32_t tile = S.tile;
+  if ((int64_t)tile >= need) break;  // every ticket has gone out
   const int64_t tbase = (int64_t)tile * SORT_TILE;
-  if (tbase >= n && tile > 0) return;  // past the data (SORT_BAD sizes its grid for the capacity)
+  if (tbase >= n && tile > 0) break;  // past the data (SORT_BAD sizes its grid for the capacity)
   const int64_t wbase = tbase + (int64_t)warp * 32 * SORT_ITEMS;
 
   unsigned long long k[SORT_ITEMS];
@@ -222,6 +233,9 @@ __global__ void __launch_bounds__(SORT_BLOCK, 2) k_onesweep(const unsigned long 
     int64_t g = (int64_t)S.gbase[dig] + i;
     kout[g] = key;
     vout[g] = S.vals[i];
+  }
+  if (!BH_SORT_PERSIST) break;
+  __syncthreads();  // S is reused by the next tile
   }
 }
 
@@ -330,9 +344,10 @@ cudaError_t launch_sort(const Workspace &W, int64_t n, cudaStream_t s, int *fina
     attr = true;
   }
   int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+  const int64_t grid = BH_SORT_PERSIST && tiles > SORT_PERSIST_GRID ? SORT_PERSIST_GRID : tiles;
   int src = 0;
   for (int pass = 0; pass < SORT_PASSES; pass++) {
-    k_onesweep<<<(unsigned)tiles, SORT_BLOCK, sizeof(SortSmem), s>>>(
+    k_onesweep<<<(unsigned)grid, SORT_BLOCK, sizeof(SortSmem), s>>>(
         W.keys[src], pass == 0 ? nullptr : W.vals[src], W.keys[src ^ 1], W.vals[src ^ 1], n, 8 * pass, W.sort_hist + pass * SORT_RADIX,
         W.sort_status + (size_t)pass * tiles * SORT_RADIX, W.sort_tilectr + pass, W.status, SORT_FULL);
     src ^= 1;
@@ -351,9 +366,10 @@ cudaError_t launch_sort_bad(const Workspace &W, int64_t tiles, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  const int64_t grid = BH_SORT_PERSIST && tiles > SORT_PERSIST_GRID ? SORT_PERSIST_GRID : tiles;
   int src = 1;
   for (int pass = 0; pass < SORT_PASSES; pass++) {
-    k_onesweep<<<(unsigned)tiles, SORT_BLOCK, sizeof(SortSmem), s>>>(
+    k_onesweep<<<(unsigned)grid, SORT_BLOCK, sizeof(SortSmem), s>>>(
         W.keys[src], W.vals[src], W.keys[src ^ 1], W.vals[src ^ 1], 0, 8 * pass, W.sort_hist + pass * SORT_RADIX,
         W.sort_status + (size_t)pass * tiles * SORT_RADIX, W.sort_tilectr + pass, W.status, SORT_BAD);
     src ^= 1;
