@@ -43,7 +43,10 @@ namespace bh {
 #define BH_WALK_UNROLL_NP2 4  // 4 targets per lane (4 vs 3, with 32-trip blocks: cfg4 walk 38.05 -> 37.75 ms, cfg5 63.99 -> 63.13)
 #endif
 #ifndef BH_WALK_UNROLL_SMALL
-#define BH_WALK_UNROLL_SMALL 3  // groups of <= 2 lanes (3 vs 2: cfg5 -2.2%, cfg3 -1.2%, cfg2 -1.4%, r1)
+#define BH_WALK_UNROLL_SMALL 4  // groups of <= 2 lanes, 2 targets per lane (3 vs 2: cfg5 -2.2%, cfg3 -1.2%, cfg2 -1.4%, r1; 4 vs 3: cfg2 -1.3%, r2zf)
+#endif
+#ifndef BH_WALK_UNROLL_NP2_L1
+#define BH_WALK_UNROLL_NP2_L1 5  // a lane's own 4 targets (code 70; 5 vs 4: cfg5 walk 63.15 -> 62.85 ms; code 69 lost 9% at 5)
 #endif
 // Accumulation: every target's contributions are summed in fp32 over blocks
 // of BH_FOLD_TRIPS loop trips of its group's walk, and each block is folded
@@ -153,7 +156,7 @@ __device__ __forceinline__ void mac_cnt_r2(uint32_t cc, float d2, float tacc, fl
 }
 // ... and no flag at all: the count is summed as rsqrt(r2m)^2 x r2 on the FMA
 // pipe (BH_MR2_FCNT: 1 +- 2^-20 for an accept, exactly 0 otherwise; rounded
-// to the integer at every flush, <= 128 terms per block: error < 2e-3)
+// to the integer at every flush, <= 160 terms per block: error < 2e-3)
 __device__ __forceinline__ void mac_r2(uint32_t cc, float d2, float tacc, float trej, uint32_t skip,
                                        uint32_t dropw, uint32_t &res, float &r2m) {
   asm("{\n\t.reg .pred pa, pc, pq;\n\t"
@@ -294,7 +297,8 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
   uint32_t trip = 0;
   if (__any_sync(full, c < Wn)) for (;;) {
 #pragma unroll
-    for (int u = 0; u < (NP == 2 ? BH_WALK_UNROLL_NP2 : GL <= 2 ? BH_WALK_UNROLL_SMALL : BH_WALK_UNROLL); u++) {
+    for (int u = 0; u < (NP == 2 ? (GL == 1 ? BH_WALK_UNROLL_NP2_L1 : BH_WALK_UNROLL_NP2)
+                                 : GL <= 2 ? BH_WALK_UNROLL_SMALL : BH_WALK_UNROLL); u++) {
       const uint32_t cc = c;
       float4 cm;
       uint4 au;
