@@ -140,20 +140,6 @@ __device__ __forceinline__ void mac_accf_r2(uint32_t cc, float d2, float tacc, f
 }
 // (2 = for 4 targets per lane only: cfg4 walk 39.5 -> 38.2 ms, cfg5 66.0 -> 65.3,
 // cfg3 0.705 -> 0.690; 2 targets per lane lost, cfg2 0.605 -> 0.623)
-// ... and the count as an integer (a predicated add in place of the float
-// flag: no FADD2 per pair, the same ALU count)
-__device__ __forceinline__ void mac_cnt_r2(uint32_t cc, float d2, float tacc, float trej, uint32_t skip,
-                                           uint32_t dropw, uint32_t &res, uint32_t &cnt, float &r2m) {
-  asm("{\n\t.reg .pred pa, pc, pq;\n\t"
-      "setp.ge.u32 pa, %3, %0;\n\t"
-      "setp.gt.and.f32 pc, %4, %5, pa;\n\t"
-      "setp.ge.and.f32 pq, %4, %6, pa;\n\t"
-      "@pq selp.b32 %0, %7, %8, pc;\n\t"
-      "@pc add.u32 %1, %1, 1;\n\t"
-      "selp.f32 %2, %4, 0f7F800000, pc;\n\t}"
-      : "+r"(res), "+r"(cnt), "=f"(r2m)
-      : "r"(cc), "f"(d2), "f"(tacc), "f"(trej), "r"(skip), "r"(dropw));
-}
 // ... and no flag at all: the count is summed as rsqrt(r2m)^2 x r2 on the FMA
 // pipe (BH_MR2_FCNT: 1 +- 2^-20 for an accept, exactly 0 otherwise; rounded
 // to the integer at every flush, <= 160 terms per block: error < 2e-3)
@@ -174,9 +160,8 @@ __device__ __forceinline__ void mac_r2(uint32_t cc, float d2, float tacc, float 
 #ifndef BH_MR2_FCNT
 #define BH_MR2_FCNT 2
 #endif
-#ifndef BH_MR2_INTCNT
-#define BH_MR2_INTCNT 0  // (1: ptxas materialises the predicates, 74 vs 66 instructions per visit)
-#endif
+// (an integer count by a predicated add instead was measured: ptxas
+// materialises the predicates, 74 vs 66 instructions per visit)
 #ifndef BH_MASK_R2
 #define BH_MASK_R2 2
 #endif
@@ -188,7 +173,7 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
   // the force mask on r2 (BH_MASK_R2, 4 targets per lane by default)
   constexpr bool MR2 = (BH_MASK_R2 == 1 || (BH_MASK_R2 == 2 && NP == 2)) && BH_EPS_FOLD && !CONT && !QUAD;
   constexpr bool MFC = MR2 && (BH_MR2_FCNT == 1 || (BH_MR2_FCNT == 2 && GL == 1));  // count = rsqrt^2 x r2
-  constexpr bool FCNT = !CONT && !(MR2 && !MFC && BH_MR2_INTCNT);  // float accept counts (flushed every BH_FOLD_TRIPS)
+  constexpr bool FCNT = !CONT;  // float accept counts, flushed every BH_FOLD_TRIPS  // float accept counts (flushed every BH_FOLD_TRIPS)
   constexpr int GT = GL * TPL;             // targets per group
   constexpr int GPB = BH_WALK_BLOCK / GL;  // groups per block
   const uint32_t full = 0xffffffffu;
@@ -330,9 +315,6 @@ __global__ void __launch_bounds__(BH_WALK_BLOCK, QUAD ? 8 : (NP == 1 ? BH_WALK_M
           if constexpr (MFC) {
             mac_r2(cc, r2A, tacc, trej, skip, dropw, res[ka], rmA);
             mac_r2(cc, r2B, tacc, trej, skip, dropw, res[kb], rmB);
-          } else if constexpr (BH_MR2_INTCNT) {
-            mac_cnt_r2(cc, r2A, tacc, trej, skip, dropw, res[ka], cnt[ka], rmA);
-            mac_cnt_r2(cc, r2B, tacc, trej, skip, dropw, res[kb], cnt[kb], rmB);
           } else {
             float accA, accB;
             mac_accf_r2(cc, r2A, tacc, trej, skip, dropw, res[ka], accA, rmA);
