@@ -52,6 +52,9 @@
 #ifndef BH_MOM_PREFETCH
 #define BH_MOM_PREFETCH 2  // (2 vs 1/3/4: best on cfg4 and on cfg5 with the containment fold)
 #endif
+#ifndef BH_MOM_WAVES
+#define BH_MOM_WAVES 4  // grid cap in blocks per SM: one resident wave at 64 registers (4 vs 8: cfg5 moments 2.684 -> 2.646 ms, cfg3 0.178 -> 0.171, cfg4 0.614 -> 0.611; 3: worse, 2: cfg5 3.44)
+#endif
 #ifndef BH_MOM_MINB
 #define BH_MOM_MINB 4  // 64 registers: 4 blocks (32 warps) per SM (the containment fold needs 66 unbounded: 3 blocks, cfg5 moments +20%)
 #endif
@@ -388,10 +391,10 @@ cudaError_t launch_moments(const Workspace &W, int64_t n, double theta, float ep
   cf.on = cont_fold;
   if (n < 2) return cudaSuccess;
   const double eps2d = BH_EPS_FOLD ? (double)eps2 : 0.0;  // the walk's fp32 eps^2, exactly
-  // grid: enough blocks for the widest level (at most n items), capped at 8
-  // waves of 148 SMs
+  // grid: enough blocks for the widest level (at most n items), capped at
+  // BH_MOM_WAVES blocks per SM (one resident wave; the items are grid-strided)
   int64_t need = (n + 255) / 256;
-  int64_t lim = 148 * 8;
+  int64_t lim = 148 * BH_MOM_WAVES;
   int grid = (int)(need < lim ? need : lim);
   if (grid < 1) grid = 1;
   for (int l = BH_MAXLEVEL; l >= 0; l--) {
