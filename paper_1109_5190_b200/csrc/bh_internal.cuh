@@ -142,7 +142,10 @@ struct Layout {
 
 // radix sort geometry (sort.cu)
 constexpr int SORT_BLOCK = 256;
-constexpr int SORT_ITEMS = 16;
+#ifndef BH_SORT_ITEMS
+#define BH_SORT_ITEMS 16
+#endif
+constexpr int SORT_ITEMS = BH_SORT_ITEMS;
 constexpr int SORT_TILE = SORT_BLOCK * SORT_ITEMS;
 constexpr int SORT_PASSES = 8;
 constexpr int SORT_RADIX = 256;
